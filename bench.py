@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""MADDNESS encode+scan throughput on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--mode exact|avg] [--impl reference]
+
+Workload (BASELINE.json metric, configs[2]): D = 512, M = 100, C = 32 (the
+CIFAR-100-classifier-shaped config), exact integer sum. Each GPU holds its own
+2^21 x 512 fp32 shard of A (4 GiB, well above the 126 MB L2, so no L2 flush is
+needed between steps). One step = one pass of the whole hot path over that
+shard: encode (Alg. 1) -> LUT scan -> dequantise, i.e. one mdn_amm call.
+Multi-GPU: one process per GPU (torchrun), the model and LUT bytes broadcast
+once over NCCL, rows sharded with no data-path collective (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = "cls100"
+METRIC = "MADDNESS encode+scan rows/s and % HBM peak (D=512,M=100,C=32), 1/2/4/8 GPUs"
+ROWS_PER_GPU = 1 << 21
+NOMINAL_HBM_GBS = 8000.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _clock_sampler(device_index):
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        return subprocess.Popen(["nvidia-smi", f"--id={device_index}", f"--query-gpu={q}",
+                                 "--format=csv,noheader,nounits", "-lms", "100"],
+                                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except Exception:
+        return None
+
+
+def _clock_summary(proc):
+    if proc is None:
+        return None
+    proc.terminate()
+    try:
+        out, _ = proc.communicate(timeout=5)
+    except Exception:
+        return None
+    sm, mx, reasons = [], 0.0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in out.strip().splitlines():
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 9:
+            continue
+        try:
+            sm.append(float(f[1]))
+            mx = max(mx, float(f[2]))
+        except ValueError:
+            continue
+        for n, v in zip(names, f[5:9]):
+            if v.lower().startswith("active"):
+                reasons.add(n)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+ORACLE_CHUNK = 16384
+
+
+def oracle_step(blk: np.ndarray, om, oluts, mode: str):
+    """One oracle pass (encode + scan + dequant) over host rows."""
+    import oracle as O
+    codes = O.encode(blk, om)
+    S = O.scan_exact(codes, oluts.Tq) if mode == "exact" else O.scan_avg(codes, oluts.Tq, oluts.U)
+    return O.dequantize(S, oluts.alpha, oluts.beta32)
+
+
+def oracle_rows_per_s(A_host: np.ndarray, om, oluts, budget_s: float, mode: str):
+    """Time the oracle (as it stands) on 16384-row chunks of host rows until
+    `budget_s` seconds of CPU work; returns (rows/s, rows, seconds)."""
+    rows, t_tot, i = 0, 0.0, 0
+    while t_tot < budget_s or i == 0:
+        s = (i * ORACLE_CHUNK) % max(1, A_host.shape[0] - ORACLE_CHUNK + 1)
+        blk = A_host[s:s + ORACLE_CHUNK]
+        t0 = time.perf_counter()
+        oracle_step(blk, om, oluts, mode)
+        t_tot += time.perf_counter() - t0
+        rows += blk.shape[0]
+        i += 1
+    return rows / t_tot, rows, t_tot
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host cores on a bounded sample
+    of the same workload (the tier's reference arm)."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle as O
+    from datagen.synth import CONFIGS, relu_W, relu_lowrank_torch
+    spec = CONFIGS[CONFIG]
+    blob = open(os.path.join(ROOT, "artifacts", f"{CONFIG}.mdnm"), "rb").read()
+    om = O.read_model(blob)
+    from datagen.synth import make_config_data
+    _, _, B = make_config_data(CONFIG, n_test=0)
+    oluts = O.make_luts(om, B, args.mode, spec.U)
+    sample = 1 << 16
+    A = relu_lowrank_torch(relu_W(CONFIG), sample, 0, "cpu").numpy()
+    rows_per_step = ORACLE_CHUNK
+    for i in range(args.warmup):
+        oracle_step(A[:rows_per_step], om, oluts, args.mode)
+    times = []
+    for i in range(args.steps):
+        s = (i * rows_per_step) % (sample - rows_per_step + 1)
+        t0 = time.perf_counter()
+        oracle_step(A[s:s + rows_per_step], om, oluts, args.mode)
+        times.append(time.perf_counter() - t0)
+    value = rows_per_step * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "cls100 (D=512, M=100, C=32), " + args.mode + " sum; oracle on "
+                   "16384-row steps from the same generator", "rows_per_step": rows_per_step},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} steps x 16384 rows of the bench generator"},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    import paper_2106_10860_b200 as mdn
+    from datagen.synth import CHUNK_ROWS, CONFIGS, make_config_data, relu_W, relu_lowrank_torch
+
+    spec = CONFIGS[CONFIG]
+    mode = mdn.MDN_SUM_EXACT if args.mode == "exact" else mdn.MDN_SUM_AVG
+    # --- model + LUTs: built once on rank 0, broadcast as bytes over NCCL -----
+    t_bcast = 0.0
+    if rank == 0:
+        model_blob = open(os.path.join(ROOT, "artifacts", f"{CONFIG}.mdnm"), "rb").read()
+        _, _, B = make_config_data(CONFIG, n_test=0)
+        m0 = mdn.mdn_model_load(model_blob, dev)
+        l0 = mdn.mdn_build_luts(m0, B, mode, spec.U)
+        luts_blob = mdn.mdn_luts_serialize(l0)
+    if ws > 1:
+        t0 = time.perf_counter()
+        sizes = torch.zeros(2, dtype=torch.int64, device="cuda")
+        if rank == 0:
+            sizes[0], sizes[1] = len(model_blob), len(luts_blob)
+        dist.broadcast(sizes, 0)
+        buf = torch.empty(int(sizes[0] + sizes[1]), dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(model_blob + luts_blob), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        host = buf.cpu().numpy().tobytes()
+        model_blob, luts_blob = host[:int(sizes[0])], host[int(sizes[0]):]
+        t_bcast = time.perf_counter() - t0
+    model = mdn.mdn_model_load(model_blob, dev)
+    luts = mdn.mdn_luts_load(luts_blob, dev)
+
+    # --- this rank's shard of A (2^21 rows, chunks rank*2 .. rank*2+1) --------
+    n = ROWS_PER_GPU
+    first_chunk = rank * (n // CHUNK_ROWS)
+    A = relu_lowrank_torch(relu_W(CONFIG), n, first_chunk, "cuda")
+    out = torch.empty((n, spec.M), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+
+    def step():
+        mdn.mdn_amm(model, luts, A, out, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clk = _clock_sampler(dev) if rank == 0 else None
+    time.sleep(0.3 if clk else 0)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for i in range(args.steps):
+        step()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    per_launch = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    elapsed_ms = ev[0].elapsed_time(ev[-1])
+    clocks = _clock_summary(clk)
+    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t_max.item())
+
+    rows_total = n * ws * args.steps
+    value = rows_total / (elapsed_ms / 1e3)
+    bytes_per_row = 4 * spec.D + 4 * spec.M
+    peak, peak_kind = _peaks()
+    avg_launch_s = statistics.mean(per_launch) / 1e3
+    achieved_gbs = n * bytes_per_row / avg_launch_s / 1e9
+
+    # --- quality (NMSE vs exact fp64 AB on 65536 rows) and the cuBLAS context point
+    nmse = None
+    cublas = None
+    if rank == 0:
+        _, _, B = make_config_data(CONFIG, n_test=0)
+        Bd = torch.from_numpy(B).cuda()
+        rows = 65536
+        exact = (A[:rows].double() @ Bd.double())
+        nmse = float(((out[:rows].double() - exact) ** 2).sum() / (exact ** 2).sum())
+        torch.backends.cuda.matmul.allow_tf32 = False
+        ref = torch.empty_like(out)
+        torch.matmul(A, Bd, out=ref)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            torch.matmul(A, Bd, out=ref)
+        e1.record()
+        torch.cuda.synchronize()
+        cublas = 3 * n / (e0.elapsed_time(e1) / 1e3)
+        del ref
+
+    # --- e2e: the same metric through the public API with HOST buffers --------
+    e2e = None
+    if rank == 0 or ws > 1:
+        ex = mdn.mdn_exec_create(model, luts, chunk_rows=1 << 17, n_slots=3)
+        A_h = A.cpu().pin_memory()
+        out_h = torch.empty((n, spec.M), dtype=torch.float32).pin_memory()
+        mdn.mdn_amm_host(ex, A_h, out_h)                      # warm-up
+        e2e_steps = max(1, min(args.steps, 3))
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            mdn.mdn_amm_host(ex, A_h, out_h)                  # synchronous: H2D + kernel + D2H
+        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if ws > 1:
+            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * ws * e2e_steps / float(t_e2e.item()), "unit": "rows/s",
+               "h2d_bytes_per_step": n * 4 * spec.D * ws, "d2h_bytes_per_step": n * 4 * spec.M * ws,
+               "steps": e2e_steps, "path": "mdn_amm_host (pinned host A -> 3-slot pipelined "
+               "H2D/kernel/D2H)"}
+        ex.close()
+        del A_h, out_h
+
+    # --- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only ---
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        om = O.read_model(model_blob)
+        oluts = O.make_luts(om, B, args.mode, spec.U)
+        A_s = A[:1 << 16].cpu().numpy()
+        v, r, t = oracle_rows_per_s(A_s, om, oluts, args.cpu_seconds, args.mode)
+        cpu = {"value": v, "unit": "rows/s", "cores": 1, "kind": "oracle",
+               "sample": f"{r} rows ({t:.1f} s) of this workload's first 65536 rows, "
+                         "numpy oracle encode + scan + dequant, single thread"}
+
+    if rank == 0:
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(f"{CONFIG}_{args.mode}")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic",
+            "config": {"workload": f"cls100: D=512, M=100, C=32, K=16, {args.mode} sum"
+                       + (f" (U={spec.U})" if args.mode == "avg" else "")
+                       + "; relu rank-64 rows, oracle-trained trees/ridge prototypes",
+                       "rows_per_gpu": n, "global_rows_per_step": n * ws,
+                       "A_bytes_per_gpu": n * 4 * spec.D,
+                       "l2": "inputs 4 GiB per GPU > 126 MB L2; no flush",
+                       "parallelism": f"row-sharded dp{ws}, model+LUT NCCL broadcast once"},
+            "pct_hbm_nominal_8tbs": achieved_gbs / NOMINAL_HBM_GBS,
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": achieved_gbs / peak, "peak_kind": peak_kind,
+                         "traffic": traffic,
+                         "algorithmic_bytes_per_launch": n * bytes_per_row,
+                         "kernel": mdn.mdn_amm_variant(model, luts, spec.D)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks,
+            "nmse_vs_exact_fp64": nmse,
+            "context": {"cublas_fp32_rows_per_s": cublas,
+                        "broadcast_s": t_bcast,
+                        "paper_cpu": "i7-4960HQ 1 thread: encode >100 GB/s logical A (L81); "
+                                     "scan 2x faster than Bolt (L447); ~100x vs exact (L465)"},
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--mode", choices=["exact", "avg"], default="exact")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,257 @@
+"""Thin Python binding of libmaddness (include/maddness.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+sm_100a kernels. There is no CPU fallback -- importing this package without
+the built ``libmaddness.so`` raises, and calls without a CUDA device fail.
+
+Names mirror the C ABI: ``mdn_model_load``, ``mdn_build_luts``,
+``mdn_luts_serialize``, ``mdn_luts_load``, ``mdn_encode``, ``mdn_scan``,
+``mdn_amm``, ``mdn_exec_create``, ``mdn_amm_host``.
+Device buffers are torch CUDA tensors (PyTorch is used for device memory and
+streams only); host buffers are numpy arrays or CPU tensors.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmaddness.so")
+
+MDN_SUM_EXACT = 0
+MDN_SUM_AVG = 1
+K = 16
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libmaddness.so not built at {LIB_PATH}; run `python -m paper_2106_10860_b200.build` "
+        "(there is no CPU fallback)")
+
+_lib = ct.CDLL(LIB_PATH)
+
+_vp, _sz, _i64, _i32 = ct.c_void_p, ct.c_size_t, ct.c_int64, ct.c_int
+_SIGS = {
+    "mdn_model_load": (_i32, [_vp, _sz, _i32, ct.POINTER(_vp), ct.POINTER(_sz)]),
+    "mdn_model_free": (None, [_vp]),
+    "mdn_model_info": (_i32, [_vp, ct.POINTER(_i32), ct.POINTER(_i32), ct.POINTER(ct.c_uint64)]),
+    "mdn_build_luts": (_i32, [_vp, _vp, _i64, _i64, _i32, _i32, ct.POINTER(_vp)]),
+    "mdn_luts_serialize": (_i32, [_vp, _vp, ct.POINTER(_sz)]),
+    "mdn_luts_load": (_i32, [_vp, _sz, _i32, ct.POINTER(_vp), ct.POINTER(_sz)]),
+    "mdn_luts_free": (None, [_vp]),
+    "mdn_luts_info": (_i32, [_vp, ct.POINTER(_i32), ct.POINTER(_i32), ct.POINTER(_i32),
+                             ct.POINTER(_i32), ct.POINTER(_i32), ct.POINTER(ct.c_float),
+                             ct.POINTER(ct.c_float), ct.POINTER(ct.c_uint64)]),
+    "mdn_encode": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
+    "mdn_scan": (_i32, [_vp, _vp, _i64, _vp, _vp, _i64, _vp]),
+    "mdn_amm": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "mdn_exec_create": (_i32, [_vp, _vp, _i64, _i32, ct.POINTER(_vp)]),
+    "mdn_exec_free": (None, [_vp]),
+    "mdn_amm_host": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64]),
+    "mdn_status_str": (ct.c_char_p, [_i32]),
+    "mdn_abi_version": (_i32, []),
+    "mdn_amm_variant": (_i32, [_vp, _vp, _i64, ct.c_char_p, _sz]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+class MdnError(RuntimeError):
+    def __init__(self, status: int, where: str, err_off=None):
+        msg = f"{where}: {_lib.mdn_status_str(status).decode()} ({status})"
+        if err_off is not None:
+            msg += f" at byte {err_off}"
+        super().__init__(msg)
+        self.status = status
+        self.err_off = err_off
+
+
+def _check(st, where, err_off=None):
+    if st != 0:
+        raise MdnError(st, where, err_off)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _dev_ptr(t, dtype_name, what):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{what} must be a CUDA torch.Tensor")
+    if str(t.dtype) != f"torch.{dtype_name}":
+        raise TypeError(f"{what} must be {dtype_name}, got {t.dtype}")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{what} must be 2-D with unit column stride")
+    return t.data_ptr()
+
+
+# --------------------------------------------------------------- handles --
+
+class Model:
+    """Opaque mdn_model handle (trees + prototypes resident on one device)."""
+
+    def __init__(self, handle, device):
+        self._h = handle
+        self.device = device
+        C, D, fp = _i32(), _i32(), ct.c_uint64()
+        _check(_lib.mdn_model_info(self._h, ct.byref(C), ct.byref(D), ct.byref(fp)), "mdn_model_info")
+        self.C, self.D, self.fingerprint = C.value, D.value, fp.value
+
+    def close(self):
+        if self._h:
+            _lib.mdn_model_free(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+class Luts:
+    """Opaque mdn_luts handle (quantised tables + alpha, beta on one device)."""
+
+    def __init__(self, handle, device):
+        self._h = handle
+        self.device = device
+        v = [_i32() for _ in range(5)]
+        a, b, fp = ct.c_float(), ct.c_float(), ct.c_uint64()
+        _check(_lib.mdn_luts_info(self._h, *[ct.byref(x) for x in v], ct.byref(a), ct.byref(b),
+                                  ct.byref(fp)), "mdn_luts_info")
+        self.C, self.M, self.mode, self.U, self.l = (x.value for x in v)
+        self.alpha, self.beta32, self.model_fingerprint = np.float32(a.value), np.float32(b.value), fp.value
+
+    def close(self):
+        if self._h:
+            _lib.mdn_luts_free(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+class Exec:
+    """Opaque mdn_exec handle: pipelined host-buffer executor (e2e path)."""
+
+    def __init__(self, handle, model, luts):
+        self._h, self._model, self._luts = handle, model, luts
+
+    def close(self):
+        if self._h:
+            _lib.mdn_exec_free(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+# ------------------------------------------------------------- functions --
+
+def mdn_model_load(buf: bytes, device: int = 0) -> Model:
+    h, off = _vp(), _sz(0)
+    st = _lib.mdn_model_load(buf, len(buf), device, ct.byref(h), ct.byref(off))
+    _check(st, "mdn_model_load", off.value if st == -3 else None)
+    return Model(h, device)
+
+
+def mdn_build_luts(model: Model, B, mode: int = MDN_SUM_EXACT, U: int = 16) -> Luts:
+    B = np.ascontiguousarray(np.asarray(B, dtype=np.float32))
+    h = _vp()
+    _check(_lib.mdn_build_luts(model._h, B.ctypes.data, B.shape[1], B.shape[1], mode, U,
+                               ct.byref(h)), "mdn_build_luts")
+    return Luts(h, model.device)
+
+
+def mdn_luts_serialize(luts: Luts) -> bytes:
+    n = _sz(0)
+    _check(_lib.mdn_luts_serialize(luts._h, None, ct.byref(n)), "mdn_luts_serialize")
+    buf = ct.create_string_buffer(n.value)
+    _check(_lib.mdn_luts_serialize(luts._h, buf, ct.byref(n)), "mdn_luts_serialize")
+    return buf.raw[:n.value]
+
+
+def mdn_luts_load(buf: bytes, device: int = 0) -> Luts:
+    h, off = _vp(), _sz(0)
+    st = _lib.mdn_luts_load(buf, len(buf), device, ct.byref(h), ct.byref(off))
+    _check(st, "mdn_luts_load", off.value if st == -3 else None)
+    return Luts(h, device)
+
+
+def mdn_encode(model: Model, A, codes, stream=None):
+    pa = _dev_ptr(A, "float32", "A")
+    pc = _dev_ptr(codes, "uint8", "codes")
+    if codes.shape != (A.shape[0], (model.C + 1) // 2) or not codes.is_contiguous():
+        raise ValueError("codes must be contiguous N x ceil(C/2)")
+    _check(_lib.mdn_encode(model._h, pa, A.shape[0], A.stride(0), pc, _stream_ptr(stream)),
+           "mdn_encode")
+    return codes
+
+
+def mdn_scan(luts: Luts, codes, sums=None, out=None, stream=None):
+    pc = _dev_ptr(codes, "uint8", "codes")
+    N = codes.shape[0]
+    ps = po = None
+    ldo = luts.M
+    if sums is not None:
+        ps = _dev_ptr(sums, "int32", "sums")
+        if sums.shape != (N, luts.M) or not sums.is_contiguous():
+            raise ValueError("sums must be contiguous N x M")
+    if out is not None:
+        po = _dev_ptr(out, "float32", "out")
+        if out.shape != (N, luts.M):
+            raise ValueError("out must be N x M")
+        ldo = out.stride(0)
+    _check(_lib.mdn_scan(luts._h, pc, N, ps, po, ldo, _stream_ptr(stream)), "mdn_scan")
+    return sums, out
+
+
+def mdn_amm(model: Model, luts: Luts, A, out, stream=None):
+    pa = _dev_ptr(A, "float32", "A")
+    po = _dev_ptr(out, "float32", "out")
+    if out.shape != (A.shape[0], luts.M):
+        raise ValueError("out must be N x M")
+    _check(_lib.mdn_amm(model._h, luts._h, pa, A.shape[0], A.stride(0), po, out.stride(0),
+                        _stream_ptr(stream)), "mdn_amm")
+    return out
+
+
+def mdn_amm_variant(model: Model, luts: Luts, lda: int) -> str:
+    buf = ct.create_string_buffer(64)
+    _check(_lib.mdn_amm_variant(model._h, luts._h, lda, buf, 64), "mdn_amm_variant")
+    return buf.value.decode()
+
+
+def mdn_exec_create(model: Model, luts: Luts, chunk_rows: int = 1 << 18, n_slots: int = 3) -> Exec:
+    h = _vp()
+    _check(_lib.mdn_exec_create(model._h, luts._h, chunk_rows, n_slots, ct.byref(h)),
+           "mdn_exec_create")
+    return Exec(h, model, luts)
+
+
+def _host_ptr(x, what):
+    if isinstance(x, np.ndarray):
+        if x.dtype != np.float32 or x.ndim != 2 or x.strides[1] != 4:
+            raise TypeError(f"{what} must be a 2-D float32 array with unit column stride")
+        return x.ctypes.data, x.strides[0] // 4, x.shape
+    import torch
+    if isinstance(x, torch.Tensor) and not x.is_cuda and x.dtype == torch.float32 and x.dim() == 2 \
+            and x.stride(1) == 1:
+        return x.data_ptr(), x.stride(0), tuple(x.shape)
+    raise TypeError(f"{what} must be host float32 (numpy or CPU tensor)")
+
+
+def mdn_amm_host(ex: Exec, A_host, out_host):
+    pa, lda, sa = _host_ptr(A_host, "A_host")
+    po, ldo, so = _host_ptr(out_host, "out_host")
+    if so[0] != sa[0]:
+        raise ValueError("row count mismatch")
+    _check(_lib.mdn_amm_host(ex._h, pa, sa[0], lda, po, ldo), "mdn_amm_host")
+    return out_host
+
+
+def abi_version() -> int:
+    return _lib.mdn_abi_version()

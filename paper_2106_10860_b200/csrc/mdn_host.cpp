@@ -1,0 +1,526 @@
+// libmaddness host side: file parsing, handle lifetime, validation, dispatch,
+// and the pipelined host-buffer executor. See include/maddness.h for the
+// contract of every entry point.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <cmath>
+#include <cstdio>
+#include <memory>
+#include <new>
+#include <vector>
+
+#include "mdn_internal.h"
+
+namespace mdn {
+
+uint64_t fnv1a64(const uint8_t* p, size_t n) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
+namespace {
+
+// Makes `dev` current for the scope of an entry point, restoring the caller's.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct Reader {
+  const uint8_t* p;
+  size_t len, off = 0;
+  bool fail = false;
+  size_t fail_off = 0;
+  template <class T>
+  T get() {
+    T v{};
+    if (off + sizeof(T) > len) {
+      if (!fail) fail_off = off;
+      fail = true;
+      return v;
+    }
+    memcpy(&v, p + off, sizeof(T));
+    off += sizeof(T);
+    return v;
+  }
+  bool need(size_t n) {
+    if (off + n > len) {
+      if (!fail) fail_off = off;
+      fail = true;
+    }
+    return !fail;
+  }
+};
+
+template <class T>
+void put(std::vector<uint8_t>& o, T v) {
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+  o.insert(o.end(), b, b + sizeof(T));
+}
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return MDN_OK;
+  if (e == cudaErrorMemoryAllocation) return MDN_ENOMEM;
+  return MDN_ECUDA;
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  return cuda_status(e);
+}
+
+bool is_pow2(int u) { return u >= 1 && (u & (u - 1)) == 0; }
+
+int set_err(size_t* err_off, size_t off, int st) {
+  if (err_off) *err_off = off;
+  return st;
+}
+
+}  // namespace
+}  // namespace mdn
+
+using namespace mdn;
+
+extern "C" {
+
+const char* mdn_status_str(int s) {
+  switch (s) {
+    case MDN_OK: return "ok";
+    case MDN_EINVAL: return "invalid argument";
+    case MDN_ESHAPE: return "shape mismatch";
+    case MDN_EFORMAT: return "bad or truncated stream";
+    case MDN_EVERSION: return "unsupported format version";
+    case MDN_ESTATE: return "luts were not built from this model";
+    case MDN_ECUDA: return "CUDA error";
+    case MDN_ENOMEM: return "out of memory";
+    case MDN_ERANGE: return "table scale exponent out of range";
+    default: return "unknown status";
+  }
+}
+
+int mdn_abi_version(void) { return MDN_ABI_VERSION; }
+
+// ----------------------------------------------------------------- model --
+
+void mdn_model_free(mdn_model* m) {
+  if (!m) return;
+  {
+    DeviceGuard g(m->device);
+    cudaFree(m->d_dims);
+    cudaFree(m->d_thr);
+    cudaFree(m->d_P);
+  }
+  delete m;
+}
+
+int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, size_t* err_off) {
+  if (!buf || !out) return MDN_EINVAL;
+  *out = nullptr;
+  Reader r{static_cast<const uint8_t*>(buf), len};
+  if (!r.need(48) || memcmp(r.p, "MDNM", 4) != 0) return set_err(err_off, 0, MDN_EFORMAT);
+  r.off = 4;
+  uint32_t ver = r.get<uint32_t>(), C = r.get<uint32_t>(), D = r.get<uint32_t>();
+  uint32_t k = r.get<uint32_t>(), flags = r.get<uint32_t>();
+  if (ver != 1) return set_err(err_off, 4, MDN_EVERSION);
+  if (k != (uint32_t)K) return set_err(err_off, 16, MDN_EINVAL);
+  if (C < 1 || C > (uint32_t)MAX_C || D < 1 || D > 65535 || C > D)
+    return set_err(err_off, 8, MDN_EINVAL);
+  std::unique_ptr<mdn_model> m(new (std::nothrow) mdn_model());
+  if (!m) return MDN_ENOMEM;
+  m->device = device;
+  m->C = (int)C;
+  m->D = (int)D;
+  m->flags = flags;
+  m->lambda = r.get<double>();
+  m->n_train = r.get<uint64_t>();
+  m->seed = r.get<uint64_t>();
+  m->h_dims.assign((size_t)C * 4, 0);
+  m->h_thr.assign((size_t)C * THR_STRIDE, 0.f);
+  for (uint32_t c = 0; c < C; ++c) {
+    size_t rec = r.off;
+    uint32_t b = r.get<uint32_t>(), e = r.get<uint32_t>();
+    for (int t = 0; t < 4; ++t) m->h_dims[c * 4 + t] = r.get<uint16_t>();
+    for (int i = 0; i < 15; ++i) m->h_thr[c * THR_STRIDE + i] = r.get<float>();
+    if (r.fail) return set_err(err_off, r.fail_off, MDN_EFORMAT);
+    if (b > e || e > D) return set_err(err_off, rec, MDN_EFORMAT);
+    for (int t = 0; t < 4; ++t)
+      if (m->h_dims[c * 4 + t] >= D) return set_err(err_off, rec + 8 + 2 * t, MDN_EINVAL);
+  }
+  size_t p_bytes = (size_t)K * C * D * sizeof(float);
+  if (!r.need(p_bytes + 8)) return set_err(err_off, r.fail_off, MDN_EFORMAT);
+  const uint8_t* P = r.p + r.off;
+  r.off += p_bytes;
+  uint64_t fp_stored = r.get<uint64_t>();
+  uint64_t fp = fnv1a64(r.p, r.off - 8);
+  if (fp != fp_stored) return set_err(err_off, r.off - 8, MDN_EFORMAT);
+  m->fingerprint = fp;
+
+  DeviceGuard g(device);
+  if (!g.ok) return MDN_ECUDA;
+  int st;
+  if ((st = dalloc(&m->d_dims, m->h_dims.size())) != MDN_OK) return st;
+  if ((st = dalloc(&m->d_thr, m->h_thr.size())) != MDN_OK) {
+    mdn_model_free(m.release());
+    return st;
+  }
+  if ((st = dalloc(&m->d_P, (size_t)K * C * D)) != MDN_OK) {
+    mdn_model_free(m.release());
+    return st;
+  }
+  cudaError_t e1 = cudaMemcpy(m->d_dims, m->h_dims.data(), m->h_dims.size() * 2, cudaMemcpyHostToDevice);
+  cudaError_t e2 = cudaMemcpy(m->d_thr, m->h_thr.data(), m->h_thr.size() * 4, cudaMemcpyHostToDevice);
+  cudaError_t e3 = cudaMemcpy(m->d_P, P, p_bytes, cudaMemcpyHostToDevice);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+    mdn_model_free(m.release());
+    return MDN_ECUDA;
+  }
+  *out = m.release();
+  return MDN_OK;
+}
+
+int mdn_model_info(const mdn_model* m, int* C, int* D, uint64_t* fp) {
+  if (!m) return MDN_EINVAL;
+  if (C) *C = m->C;
+  if (D) *D = m->D;
+  if (fp) *fp = m->fingerprint;
+  return MDN_OK;
+}
+
+// ------------------------------------------------------------------ luts --
+
+void mdn_luts_free(mdn_luts* l) {
+  if (!l) return;
+  {
+    DeviceGuard g(l->device);
+    cudaFree(l->d_tq);
+    cudaFree(l->d_words);
+  }
+  delete l;
+}
+
+static int alloc_luts(int device, int C, int M, mdn_luts** out) {
+  std::unique_ptr<mdn_luts> l(new (std::nothrow) mdn_luts());
+  if (!l) return MDN_ENOMEM;
+  l->device = device;
+  l->C = C;
+  l->M = M;
+  l->W = (M + 3) / 4;
+  int st;
+  if ((st = dalloc(&l->d_tq, (size_t)C * K * M)) != MDN_OK) return st;
+  if ((st = dalloc(&l->d_words, (size_t)C * l->W * K)) != MDN_OK) {
+    cudaFree(l->d_tq);
+    return st;
+  }
+  *out = l.release();
+  return MDN_OK;
+}
+
+int mdn_build_luts(const mdn_model* m, const float* B, int64_t M, int64_t ldb, int mode, int U,
+                   mdn_luts** out) {
+  if (!m || !B || !out || M < 1 || M > 4096 || ldb < M) return MDN_EINVAL;
+  if (mode != MDN_SUM_EXACT && mode != MDN_SUM_AVG) return MDN_EINVAL;
+  if (mode == MDN_SUM_AVG && (!is_pow2(U) || m->C % U != 0 || U > 64)) return MDN_EINVAL;
+  if (mode == MDN_SUM_EXACT) U = 1;
+  *out = nullptr;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  const int C = m->C, D = m->D;
+  mdn_luts* l = nullptr;
+  int st = alloc_luts(m->device, C, (int)M, &l);
+  if (st != MDN_OK) return st;
+  l->mode = mode;
+  l->U = U;
+  l->model_fp = m->fingerprint;
+  // Host B (D x M, ldb) -> dense device copy.
+  std::vector<float> hb((size_t)D * M);
+  for (int64_t j = 0; j < D; ++j) memcpy(&hb[j * M], B + j * ldb, M * sizeof(float));
+  float* dB = nullptr;
+  double *dT = nullptr, *dDelta = nullptr, *dRange = nullptr;
+  LutScalars* dScal = nullptr;
+  LutScalars hs{};
+  cudaError_t e = cudaSuccess;
+  if ((st = dalloc(&dB, hb.size())) || (st = dalloc(&dT, (size_t)K * C * M)) ||
+      (st = dalloc(&dDelta, C)) || (st = dalloc(&dRange, C)) || (st = dalloc(&dScal, 1))) {
+    goto fail;
+  }
+  e = cudaMemcpy(dB, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = build_tables_dev(m->d_P, dB, C, D, (int)M, mode == MDN_SUM_AVG ? U : 0, dT, dDelta, dRange,
+                         dScal, l->d_tq, l->d_words, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(&hs, dScal, sizeof(hs), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) {
+    l->delta.resize(C);
+    e = cudaMemcpy(l->delta.data(), dDelta, C * sizeof(double), cudaMemcpyDeviceToHost);
+  }
+  if (e != cudaSuccess) {
+    st = cuda_status(e);
+    goto fail;
+  }
+  if (hs.err) {
+    st = MDN_ERANGE;
+    goto fail;
+  }
+  l->l = hs.l;
+  l->alpha = hs.alpha;
+  l->beta32 = hs.beta32;
+  cudaFree(dB);
+  cudaFree(dT);
+  cudaFree(dDelta);
+  cudaFree(dRange);
+  cudaFree(dScal);
+  *out = l;
+  return MDN_OK;
+fail:
+  cudaFree(dB);
+  cudaFree(dT);
+  cudaFree(dDelta);
+  cudaFree(dRange);
+  cudaFree(dScal);
+  mdn_luts_free(l);
+  return st;
+}
+
+int mdn_luts_serialize(const mdn_luts* l, void* buf, size_t* len) {
+  if (!l || !len) return MDN_EINVAL;
+  size_t tq = (size_t)l->C * K * l->M;
+  size_t need = 4 + 6 * 4 + 4 + 4 + 4 + 8 + 8 * (size_t)l->C + tq + 8;
+  if (!buf) {
+    *len = need;
+    return MDN_OK;
+  }
+  if (*len < need) return MDN_EINVAL;
+  std::vector<uint8_t> o;
+  o.reserve(need);
+  o.insert(o.end(), {'M', 'D', 'N', 'L'});
+  put<uint32_t>(o, 1);
+  put<uint32_t>(o, l->C);
+  put<uint32_t>(o, l->M);
+  put<uint32_t>(o, K);
+  put<uint32_t>(o, l->mode);
+  put<uint32_t>(o, l->U);
+  put<int32_t>(o, l->l);
+  put<float>(o, l->alpha);
+  put<float>(o, l->beta32);
+  put<uint64_t>(o, l->model_fp);
+  for (double d : l->delta) put<double>(o, d);
+  size_t at = o.size();
+  o.resize(at + tq);
+  {
+    DeviceGuard g(l->device);
+    if (cudaMemcpy(o.data() + at, l->d_tq, tq, cudaMemcpyDeviceToHost) != cudaSuccess) return MDN_ECUDA;
+  }
+  put<uint64_t>(o, fnv1a64(o.data(), o.size()));
+  memcpy(buf, o.data(), o.size());
+  *len = o.size();
+  return MDN_OK;
+}
+
+int mdn_luts_load(const void* buf, size_t len, int device, mdn_luts** out, size_t* err_off) {
+  if (!buf || !out) return MDN_EINVAL;
+  *out = nullptr;
+  Reader r{static_cast<const uint8_t*>(buf), len};
+  if (!r.need(52) || memcmp(r.p, "MDNL", 4) != 0) return set_err(err_off, 0, MDN_EFORMAT);
+  r.off = 4;
+  uint32_t ver = r.get<uint32_t>(), C = r.get<uint32_t>(), M = r.get<uint32_t>();
+  uint32_t k = r.get<uint32_t>(), mode = r.get<uint32_t>(), U = r.get<uint32_t>();
+  if (ver != 1) return set_err(err_off, 4, MDN_EVERSION);
+  if (k != (uint32_t)K || C < 1 || C > (uint32_t)MAX_C || M < 1 || M > 4096 || mode > 1 ||
+      !is_pow2((int)U) || C % U != 0)
+    return set_err(err_off, 8, MDN_EINVAL);
+  int32_t lexp = r.get<int32_t>();
+  float alpha = r.get<float>(), beta = r.get<float>();
+  uint64_t mfp = r.get<uint64_t>();
+  std::vector<double> delta(C);
+  for (uint32_t c = 0; c < C; ++c) delta[c] = r.get<double>();
+  size_t tq = (size_t)C * K * M;
+  if (r.fail || !r.need(tq + 8)) return set_err(err_off, r.fail_off, MDN_EFORMAT);
+  const uint8_t* tqp = r.p + r.off;
+  r.off += tq;
+  uint64_t fp_stored = r.get<uint64_t>();
+  if (fnv1a64(r.p, r.off - 8) != fp_stored) return set_err(err_off, r.off - 8, MDN_EFORMAT);
+  DeviceGuard g(device);
+  if (!g.ok) return MDN_ECUDA;
+  mdn_luts* l = nullptr;
+  int st = alloc_luts(device, (int)C, (int)M, &l);
+  if (st != MDN_OK) return st;
+  l->mode = (int)mode;
+  l->U = (int)U;
+  l->l = lexp;
+  l->alpha = alpha;
+  l->beta32 = beta;
+  l->model_fp = mfp;
+  l->delta = delta;
+  cudaError_t e = cudaMemcpy(l->d_tq, tqp, tq, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = pack_words_dev(l->d_tq, l->C, l->M, l->d_words, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    mdn_luts_free(l);
+    return cuda_status(e);
+  }
+  *out = l;
+  return MDN_OK;
+}
+
+int mdn_luts_info(const mdn_luts* l, int* C, int* M, int* mode, int* U, int* lexp, float* alpha,
+                  float* beta32, uint64_t* mfp) {
+  if (!l) return MDN_EINVAL;
+  if (C) *C = l->C;
+  if (M) *M = l->M;
+  if (mode) *mode = l->mode;
+  if (U) *U = l->U;
+  if (lexp) *lexp = l->l;
+  if (alpha) *alpha = l->alpha;
+  if (beta32) *beta32 = l->beta32;
+  if (mfp) *mfp = l->model_fp;
+  return MDN_OK;
+}
+
+// -------------------------------------------------------------- hot path --
+
+int mdn_encode(const mdn_model* m, const float* A, int64_t N, int64_t lda, uint8_t* codes,
+               void* stream) {
+  if (!m || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!A || !codes || lda < m->D) return MDN_EINVAL;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  return cuda_status(launch_encode(m->trees(), A, N, lda, codes, (cudaStream_t)stream));
+}
+
+int mdn_scan(const mdn_luts* l, const uint8_t* codes, int64_t N, int32_t* sums, float* out,
+             int64_t ldo, void* stream) {
+  if (!l || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!codes || (!sums && !out) || (out && ldo < l->M)) return MDN_EINVAL;
+  DeviceGuard g(l->device);
+  if (!g.ok) return MDN_ECUDA;
+  return cuda_status(launch_scan(l->dev(), codes, N, sums, out, ldo, (cudaStream_t)stream));
+}
+
+int mdn_amm(const mdn_model* m, const mdn_luts* l, const float* A, int64_t N, int64_t lda,
+            float* out, int64_t ldo, void* stream) {
+  if (!m || !l || N < 0) return MDN_EINVAL;
+  if (l->C != m->C) return MDN_ESHAPE;
+  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  if (l->device != m->device) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!A || !out || lda < m->D || ldo < l->M) return MDN_EINVAL;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  return cuda_status(launch_amm(m->trees(), l->dev(), A, N, lda, out, ldo, (cudaStream_t)stream));
+}
+
+int mdn_amm_variant(const mdn_model* m, const mdn_luts* l, int64_t lda, char* buf, size_t len) {
+  if (!m || !l || !buf || len == 0) return MDN_EINVAL;
+  // Report for a 16-B aligned A / out with ldo == M.
+  const char* name = amm_variant_name(m->trees(), l->dev(), reinterpret_cast<const float*>(256),
+                                      lda, reinterpret_cast<const float*>(256), l->M);
+  snprintf(buf, len, "%s", name);
+  return MDN_OK;
+}
+
+// ------------------------------------------------------ host executor (e2e) --
+
+struct mdn_exec {
+  const mdn_model* model;
+  const mdn_luts* luts;
+  int device;
+  int64_t chunk;
+  int n_slots;
+  std::vector<cudaStream_t> streams;
+  std::vector<float*> dA, dOut;
+};
+
+void mdn_exec_free(mdn_exec* x) {
+  if (!x) return;
+  {
+    DeviceGuard g(x->device);
+    for (auto s : x->streams) cudaStreamDestroy(s);
+    for (auto p : x->dA) cudaFree(p);
+    for (auto p : x->dOut) cudaFree(p);
+  }
+  delete x;
+}
+
+int mdn_exec_create(const mdn_model* m, const mdn_luts* l, int64_t chunk_rows, int n_slots,
+                    mdn_exec** out) {
+  if (!m || !l || !out || chunk_rows < 1 || n_slots < 1 || n_slots > 8) return MDN_EINVAL;
+  if (l->C != m->C) return MDN_ESHAPE;
+  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  *out = nullptr;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  std::unique_ptr<mdn_exec> x(new (std::nothrow) mdn_exec());
+  if (!x) return MDN_ENOMEM;
+  x->model = m;
+  x->luts = l;
+  x->device = m->device;
+  x->chunk = chunk_rows;
+  x->n_slots = n_slots;
+  for (int i = 0; i < n_slots; ++i) {
+    cudaStream_t s;
+    float *a = nullptr, *o = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      mdn_exec_free(x.release());
+      return MDN_ECUDA;
+    }
+    x->streams.push_back(s);
+    int st = dalloc(&a, (size_t)chunk_rows * m->D);
+    if (st == MDN_OK) st = dalloc(&o, (size_t)chunk_rows * l->M);
+    x->dA.push_back(a);
+    x->dOut.push_back(o);
+    if (st != MDN_OK) {
+      mdn_exec_free(x.release());
+      return st;
+    }
+  }
+  *out = x.release();
+  return MDN_OK;
+}
+
+int mdn_amm_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
+  if (!x || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  const int D = x->model->D, M = x->luts->M;
+  if (!A || !out || lda < D || ldo < M) return MDN_EINVAL;
+  DeviceGuard g(x->device);
+  if (!g.ok) return MDN_ECUDA;
+  cudaError_t e = cudaSuccess;
+  int64_t nchunks = (N + x->chunk - 1) / x->chunk;
+  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
+    int s = (int)(q % x->n_slots);
+    cudaStream_t st = x->streams[s];
+    int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
+    // Stream order serialises reuse of slot s: H2D(q) waits for D2H(q - n_slots).
+    e = cudaMemcpy2DAsync(x->dA[s], D * sizeof(float), A + r0 * lda, lda * sizeof(float),
+                          D * sizeof(float), n, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) break;
+    e = launch_amm(x->model->trees(), x->luts->dev(), x->dA[s], n, D, x->dOut[s], M, st);
+    if (e != cudaSuccess) break;
+    e = cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
+                          M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
+  }
+  for (auto s : x->streams) {
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+  }
+  return cuda_status(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// Internal declarations shared by the host side and the kernels of libmaddness.
+// (Product code only; nothing here is shared with the oracle.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/maddness.h"
+
+namespace mdn {
+
+constexpr int K = MDN_K;           // leaves per tree
+constexpr int THR_STRIDE = 16;     // 15 heap-ordered thresholds + 1 pad per codebook
+constexpr int MAX_C = 256;         // S <= 255 * C must fit the 16-bit SWAR lanes
+
+// Tree parameters as the kernels consume them (device).
+struct TreesDev {
+  const uint16_t* dims;  // [C][4] global column of each level's split
+  const float* thr;      // [C][16] heap order, pad slot 15 unused
+  int C;
+  int D;
+};
+
+// Quantised tables as the kernels consume them (device).
+struct LutsDev {
+  const uint8_t* tq;     // canonical [C][16][M]
+  const uint32_t* words; // scan layout [C][W][16]: word (c,w,k) = Tq[c][k][4w..4w+3]
+  int C, M, W;
+  int U;                 // 0 = exact sum; else averaging block size (power of two)
+  float alpha_eff;       // alpha (exact) or alpha * U (avg): out = alpha_eff * S' + beta
+  float beta32;
+};
+
+// Kernel entry points (mdn_kernels.cu / mdn_luts.cu / mdn_amm_tma.cu).
+cudaError_t launch_encode(const TreesDev& t, const float* A, int64_t N, int64_t lda,
+                          uint8_t* codes, cudaStream_t s);
+cudaError_t launch_scan(const LutsDev& l, const uint8_t* codes, int64_t N, int32_t* sums,
+                        float* out, int64_t ldo, cudaStream_t s);
+cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
+                       int64_t lda, float* out, int64_t ldo, cudaStream_t s);
+const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
+                             const float* out, int64_t ldo);
+
+// LUT build (device fp64), writes tq/words and the scalars.
+struct LutScalars {
+  int l;
+  int err;        // 1 = |l| > 100
+  float alpha;
+  float beta32;
+};
+cudaError_t build_tables_dev(const float* dP, const float* dB, int C, int D, int M,
+                             int U_or_0, double* dT, double* dDelta, double* dRange,
+                             LutScalars* dScal, uint8_t* dTq, uint32_t* dWords,
+                             cudaStream_t s);
+cudaError_t pack_words_dev(const uint8_t* dTq, int C, int M, uint32_t* dWords, cudaStream_t s);
+
+uint64_t fnv1a64(const uint8_t* p, size_t n);
+
+}  // namespace mdn
+
+struct mdn_model {
+  int device;
+  int C, D;
+  uint32_t flags;
+  double lambda;
+  uint64_t n_train, seed, fingerprint;
+  std::vector<uint16_t> h_dims;   // [C][4]
+  std::vector<float> h_thr;       // [C][16]
+  uint16_t* d_dims = nullptr;
+  float* d_thr = nullptr;
+  float* d_P = nullptr;           // [16C][D]
+  mdn::TreesDev trees() const { return {d_dims, d_thr, C, D}; }
+};
+
+struct mdn_luts {
+  int device;
+  int C, M, W, mode, U, l;
+  float alpha, beta32;
+  uint64_t model_fp;
+  std::vector<double> delta;
+  uint8_t* d_tq = nullptr;       // [C][16][M]
+  uint32_t* d_words = nullptr;   // [C][W][16]
+  mdn::LutsDev dev() const {
+    float ae = mode == MDN_SUM_AVG ? alpha * (float)U : alpha;   // exact: power of two
+    return {d_tq, d_words, C, M, W, mode == MDN_SUM_AVG ? U : 0, ae, beta32};
+  }
+};

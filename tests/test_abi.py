@@ -1,0 +1,116 @@
+"""CPU checks of the C-ABI library: it builds for sm_100a, loads, exports every
+symbol include/maddness.h declares, and rejects malformed inputs before any
+device work (no compute calls without a GPU)."""
+import ctypes as ct
+import os
+import re
+import struct
+
+import pytest
+
+from helpers import ROOT, model_bytes
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2106_10860_b200.build import build
+    path = build()
+    return ct.CDLL(path)
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "maddness.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mdn_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _declared()
+    assert len(names) >= 17
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_binding_exposes_same_names():
+    import paper_2106_10860_b200 as mdn
+    for n in _declared():
+        assert n in mdn.EXPORTED
+    for n in ("mdn_model_load", "mdn_build_luts", "mdn_luts_serialize", "mdn_luts_load",
+              "mdn_encode", "mdn_scan", "mdn_amm", "mdn_exec_create", "mdn_amm_host"):
+        assert callable(getattr(mdn, n))
+
+
+def test_sm100a_cubin_present():
+    """The library carries sm_100a SASS (nvcc -gencode arch=compute_100a,code=sm_100a)."""
+    import subprocess
+    from paper_2106_10860_b200 import LIB_PATH
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings(lib):
+    lib.mdn_status_str.restype = ct.c_char_p
+    assert lib.mdn_status_str(0) == b"ok"
+    assert b"stream" in lib.mdn_status_str(-3)
+    assert lib.mdn_abi_version() == 1
+
+
+def _load(lib, blob):
+    h, off = ct.c_void_p(), ct.c_size_t(0)
+    lib.mdn_model_load.argtypes = [ct.c_void_p, ct.c_size_t, ct.c_int, ct.POINTER(ct.c_void_p),
+                                   ct.POINTER(ct.c_size_t)]
+    st = lib.mdn_model_load(blob, len(blob), 0, ct.byref(h), ct.byref(off))
+    return st, off.value
+
+
+def test_model_parser_errors(lib):
+    blob = model_bytes("tiny")
+    assert _load(lib, b"XXXX" + blob[4:]) == (-3, 0)
+    st, off = _load(lib, blob[:100])
+    assert st == -3 and off > 0
+    assert _load(lib, blob[:4] + struct.pack("<I", 7) + blob[8:])[0] == -4
+    bad = bytearray(blob)
+    bad[-100] ^= 0xFF                               # inside P: only the fingerprint sees it
+    st, off = _load(lib, bytes(bad))
+    assert st == -3 and off == len(blob) - 8
+    bad = bytearray(blob)
+    bad[48 + 2 * 76] ^= 0xFF                        # codebook 2 sub_begin > sub_end
+    assert _load(lib, bytes(bad)) == (-3, 48 + 2 * 76)
+    bad = bytearray(blob)
+    struct.pack_into("<H", bad, 48 + 8, 9999)       # split dim >= D
+    assert _load(lib, bytes(bad))[0] in (-1, -3)
+
+
+def test_luts_parser_errors(lib):
+    h, off = ct.c_void_p(), ct.c_size_t(0)
+    lib.mdn_luts_load.argtypes = [ct.c_void_p, ct.c_size_t, ct.c_int, ct.POINTER(ct.c_void_p),
+                                  ct.POINTER(ct.c_size_t)]
+    assert lib.mdn_luts_load(b"MDNX" + b"\0" * 60, 64, 0, ct.byref(h), ct.byref(off)) == -3
+    hdr = b"MDNL" + struct.pack("<6I", 2, 4, 4, 16, 0, 1) + b"\0" * 40
+    assert lib.mdn_luts_load(hdr, len(hdr), 0, ct.byref(h), ct.byref(off)) == -4
+    hdr = b"MDNL" + struct.pack("<6I", 1, 4, 4, 16, 1, 3) + b"\0" * 40   # U not pow2
+    assert lib.mdn_luts_load(hdr, len(hdr), 0, ct.byref(h), ct.byref(off)) == -1
+
+
+def test_null_and_shape_guards(lib):
+    lib.mdn_encode.argtypes = [ct.c_void_p, ct.c_void_p, ct.c_int64, ct.c_int64, ct.c_void_p,
+                               ct.c_void_p]
+    assert lib.mdn_encode(None, None, 1, 1, None, None) == -1
+    lib.mdn_amm.argtypes = [ct.c_void_p] * 3 + [ct.c_int64] * 2 + [ct.c_void_p, ct.c_int64,
+                                                                   ct.c_void_p]
+    assert lib.mdn_amm(None, None, None, 1, 1, None, 1, None) == -1
+
+
+def test_binding_rejects_host_tensors():
+    import numpy as np
+    import torch
+
+    import paper_2106_10860_b200 as mdn
+
+    class Fake:
+        C, D, _h = 4, 32, None
+    with pytest.raises(TypeError):
+        mdn.mdn_encode(Fake(), torch.zeros(4, 32), torch.zeros(4, 2, dtype=torch.uint8))
+    with pytest.raises(TypeError):
+        mdn._host_ptr(np.zeros((2, 2), np.float64), "A_host")
