@@ -1,0 +1,633 @@
+// Fast sm_100a kernels for the MADDNESS hot path.
+//
+// k_amm_ws: the fused g + f + dequant (mdn_amm) and the encode-only variant
+// (mdn_encode). One persistent CTA per SM, warp-specialised:
+//
+//   warp 0          TMA producer: 2-D tensor copies of A row tiles into a ring
+//                   of NS shared-memory stages (mbarrier complete_tx)
+//   warps 1..E      encoders: Algorithm 1 on every
+//                   (row, codebook) of a stage, fp32 compares against thresholds
+//                   resident in shared memory; packed 4-bit codes go to a ring
+//                   of NB code tiles in shared memory (never to HBM)
+//   warps E+1..E+S  scanners: one row per thread; the C x 16 x M uint8 tables
+//                   stay resident in shared memory as 32-bit words holding 4
+//                   output columns ("f"; the paper's column-pair
+//                   fusion, App. D, generalised to 4 columns per lookup);
+//                   exact sums in 2 x 16-bit SWAR lanes, or the App. D
+//                   averaging tree with __vavgu4 (L335, L697-706); then
+//                   out = alpha * S + beta (Eq. 1) and coalescing-friendly
+//                   128-bit stores.
+//
+// Stage layout: A rows [y, y + R) are fetched as nslab boxes of
+// (SW + 4) x R floats (slab k covers columns [k SW, k SW + SW + 4)); the 4
+// extra columns pad each row to a pitch of SW + 4 words (== 4 mod 32 for
+// SW = 128 or 32), which spreads the encoders' per-row reads over banks; the
+// tail beyond column D and rows beyond N are zero-filled by the TMA unit.
+//
+// k_scan_fast: mdn_scan from packed codes in HBM, thread per row, tables in
+// shared memory.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "mdn_internal.h"
+
+namespace mdn {
+namespace fast {
+
+constexpr int E_WARPS = 2;               // encoder warps (fused kernel)
+constexpr int S_WARPS = 8;               // scanner warps
+constexpr int BR = S_WARPS * 32;         // rows per tile
+constexpr int NB = 3;                    // code ring depth (tiles)
+constexpr int NS_MAX = 8;                // A stage ring depth cap
+constexpr int THREADS = 32 * (1 + E_WARPS + S_WARPS);
+constexpr int E_WARPS_ENC = 8;           // encoder warps (encode-only kernel)
+constexpr int THREADS_ENC = 32 * (1 + E_WARPS_ENC);
+constexpr int BAR_BYTES = 256;
+
+struct Params {
+  int64_t N;
+  int64_t n_tiles;
+  int64_t ldo;
+  int D, SW, nslab, R, NS;
+  int slab_words;                 // shared-memory words per slab (128-B aligned)
+  int M;
+  float alpha_eff, beta32;
+  const uint32_t* lut;            // global [C][W][16]
+  const uint16_t* dims;           // global [C][4]
+  const float* thr;               // global [C][16]
+  float* out;
+  uint8_t* codes;                 // encode-only output
+};
+
+// ------------------------------------------------------------ PTX helpers --
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  const uint32_t a = su32(b);
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+
+// ------------------------------------------------------------ scan core --
+
+// Accumulate the W table words of every codebook for one row.
+//   words(g): the g-th 32-bit word of the row's packed codes (8 codes, low
+//   nibble first; for C < 8 only the low 4C bits are used).
+// Exact mode (U == 0): ae[w] / ao[w] hold the even / odd output columns of
+// word w in two 16-bit lanes (S <= 255 C < 2^16 for C <= 256).
+// Averaging mode: per block of U consecutive codebooks the halves-recursion
+// tree of rounded averages (mu(a,b) = (a+b+1)>>1 per byte, __vavgu4), and the
+// block results are summed exactly (App. D, reading R16/R17).
+template <int C, int W, int U, class Words>
+__device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Words words,
+                                          uint32_t (&ae)[W], uint32_t (&ao)[W]) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) ae[w] = ao[w] = 0u;
+  if constexpr (U == 0) {
+    constexpr int G = C >= 8 ? 8 : C;
+#pragma unroll 1
+    for (int g = 0; g < C / G; ++g) {
+      const uint32_t cw = words(g);
+      const uint32_t* lg = lut + g * G * W * 16;
+#pragma unroll
+      for (int i = 0; i < G; i += 2) {
+        const uint32_t* p0 = lg + (i * W) * 16 + ((cw >> (4 * i)) & 15u);
+        const uint32_t* p1 = lg + ((i + 1) * W) * 16 + ((cw >> (4 * i + 4)) & 15u);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const uint32_t a = p0[w * 16], b = p1[w * 16];
+          ae[w] += (a & 0x00FF00FFu) + (b & 0x00FF00FFu);
+          ao[w] += __byte_perm(a, 0u, 0x4341) + __byte_perm(b, 0u, 0x4341);
+        }
+      }
+    }
+  } else {
+    static_assert((U & (U - 1)) == 0 && C % U == 0, "U must be a power of two dividing C");
+#pragma unroll 1
+    for (int blk = 0; blk < C / U; ++blk) {
+      const uint32_t* p[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const int c = blk * U + i;  // runtime blk, static i
+        uint32_t cw;
+        if constexpr (U >= 8) {
+          cw = words(blk * (U / 8) + i / 8);
+          p[i] = lut + (c * W) * 16 + ((cw >> (4 * (i % 8))) & 15u);
+        } else {
+          const int cc = blk * U + i;
+          cw = words(cc >> 3);
+          p[i] = lut + (c * W) * 16 + ((cw >> (4 * (cc & 7))) & 15u);
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint32_t v[U];
+#pragma unroll
+        for (int i = 0; i < U; ++i) v[i] = p[i][w * 16];
+#pragma unroll
+        for (int s = 1; s < U; s *= 2)
+#pragma unroll
+          for (int i = 0; i < U; i += 2 * s) v[i] = __vavgu4(v[i], v[i + s]);
+        ae[w] += v[0] & 0x00FF00FFu;
+        ao[w] += __byte_perm(v[0], 0u, 0x4341);
+      }
+    }
+  }
+}
+
+// out[m] = fl32(alpha_eff * S'[m] + beta32): S' < 2^16 is exact in fp32 and
+// alpha_eff a power of two, so the FMA's single rounding equals the oracle's.
+template <int W, bool VEC>
+__device__ __forceinline__ void store_row(float* __restrict__ o, int M, const uint32_t (&ae)[W],
+                                          const uint32_t (&ao)[W], float a, float b) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    float4 f;
+    f.x = __fmaf_rn(a, (float)(ae[w] & 0xFFFFu), b);
+    f.y = __fmaf_rn(a, (float)(ao[w] & 0xFFFFu), b);
+    f.z = __fmaf_rn(a, (float)(ae[w] >> 16), b);
+    f.w = __fmaf_rn(a, (float)(ao[w] >> 16), b);
+    if constexpr (VEC) {
+      *reinterpret_cast<float4*>(o + 4 * w) = f;
+    } else {
+      const int m = 4 * w;
+      if (m + 0 < M) o[m + 0] = f.x;
+      if (m + 1 < M) o[m + 1] = f.y;
+      if (m + 2 < M) o[m + 2] = f.z;
+      if (m + 3 < M) o[m + 3] = f.w;
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void store_sums(int32_t* __restrict__ o, int M, int scale,
+                                           const uint32_t (&ae)[W], const uint32_t (&ao)[W]) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const int m = 4 * w;
+    const int v[4] = {(int)(ae[w] & 0xFFFFu), (int)(ao[w] & 0xFFFFu), (int)(ae[w] >> 16),
+                      (int)(ao[w] >> 16)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (m + i < M) o[m + i] = v[i] * scale;
+  }
+}
+
+// ------------------------------------------------------------ fused kernel --
+
+template <int C>
+__device__ __forceinline__ uint32_t encode_group(const float* __restrict__ rowp,
+                                                 const int* __restrict__ s_off,
+                                                 const float* __restrict__ s_thr, int c0, int G) {
+  uint32_t word = 0;
+#pragma unroll
+  for (int i = 0; i < (C >= 8 ? 8 : C); ++i) {
+    const int c = c0 + i;
+    const int4 o = *reinterpret_cast<const int4*>(s_off + 4 * c);
+    const float x0 = rowp[o.x], x1 = rowp[o.y], x2 = rowp[o.z], x3 = rowp[o.w];
+    const float* th = s_thr + 16 * c;
+    // Algorithm 1: i <- 2i - 1 + [x_{j^t} >= v^t_i]  (0-based: p <- 2p + b)
+    uint32_t p = x0 >= th[0] ? 1u : 0u;
+    p = 2u * p + (x1 >= th[1 + p] ? 1u : 0u);
+    p = 2u * p + (x2 >= th[3 + p] ? 1u : 0u);
+    p = 2u * p + (x3 >= th[7 + p] ? 1u : 0u);
+    word |= p << (4 * i);
+  }
+  return word;
+}
+
+template <int C, int W, int U, bool VEC, bool ENC_ONLY>
+__global__ void __launch_bounds__(ENC_ONLY ? THREADS_ENC : THREADS, 1)
+    k_amm_ws(const __grid_constant__ CUtensorMap tmap, const Params p) {
+  constexpr int G = C >= 8 ? 8 : C;      // codebooks per encoder unit (one code word)
+  constexpr int NG = C / G;
+  constexpr int CBW = NG;                // code words per row
+  constexpr int EW = ENC_ONLY ? E_WARPS_ENC : E_WARPS;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + NS_MAX;
+  uint64_t* cfull = empty + NS_MAX;
+  uint64_t* cempty = cfull + NB;
+  // Carve with integer offsets from `smem` so every pointer stays provably in
+  // the shared window (plain LDS/STS, no generic loads).
+  constexpr int OFF_THR = BAR_BYTES;
+  constexpr int OFF_OFF = OFF_THR + 16 * C * 4;
+  constexpr int OFF_LUT = (OFF_OFF + 4 * C * 4 + 15) & ~15;
+  constexpr int OFF_CODES = OFF_LUT + (ENC_ONLY ? 0 : C * W * 16 * 4);
+  constexpr int OFF_STAGE = (OFF_CODES + (ENC_ONLY ? 0 : NB * BR * CBW * 4) + 127) & ~127;
+  float* s_thr = reinterpret_cast<float*>(smem + OFF_THR);
+  int* s_off = reinterpret_cast<int*>(smem + OFF_OFF);
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
+  uint32_t* s_codes = reinterpret_cast<uint32_t*>(smem + OFF_CODES);
+  float* s_stage = reinterpret_cast<float*>(smem + OFF_STAGE);
+  const int tid = threadIdx.x;
+  const int pitch = p.SW + 4;
+  const int stage_words = p.nslab * p.slab_words;
+
+  // ---- setup: trees, split-dim offsets, tables, barriers ----
+  for (int i = tid; i < 16 * C; i += blockDim.x) s_thr[i] = p.thr[i];
+  for (int i = tid; i < 4 * C; i += blockDim.x) {
+    const int d = p.dims[i];
+    s_off[i] = (d / p.SW) * p.slab_words + (d % p.SW);
+  }
+  if constexpr (!ENC_ONLY) {
+    const uint4* src = reinterpret_cast<const uint4*>(p.lut);
+    uint4* dst = reinterpret_cast<uint4*>(s_lut);
+    for (int i = tid; i < C * W * 4; i += blockDim.x) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < p.NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], EW * 32);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&cfull[b], EW * 32);
+      mbar_init(&cempty[b], S_WARPS * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  __syncthreads();
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int stages_per_tile = BR / p.R;
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(p.nslab * p.R * pitch * 4);
+      uint32_t q = 0;
+      for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        for (int st = 0; st < stages_per_tile; ++st, ++q) {
+          const int s = q % p.NS;
+          mbar_wait(&empty[s], ((q / p.NS) & 1u) ^ 1u);
+          const int64_t y = tile * BR + (int64_t)st * p.R;
+          if (y >= p.N) {            // stage entirely past the last row: nothing to fetch
+            mbar_arrive(&full[s]);
+            continue;
+          }
+          mbar_arrive_tx(&full[s], bytes);
+          float* dst = s_stage + (size_t)s * stage_words;
+          for (int k = 0; k < p.nslab; ++k)
+            tma_load_2d(dst + k * p.slab_words, &tmap, k * p.SW, (int)y, &full[s]);
+        }
+      }
+    }
+  } else if (warp <= EW) {
+    // ---------------- encoders ----------------
+    const int etid = tid - 32;
+    uint32_t q = 0, z = 0;
+    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++z) {
+      const int b = z % NB;
+      if constexpr (!ENC_ONLY) mbar_wait(&cempty[b], ((z / NB) & 1u) ^ 1u);
+      for (int st = 0; st < stages_per_tile; ++st, ++q) {
+        const int s = q % p.NS;
+        mbar_wait(&full[s], (q / p.NS) & 1u);
+        const float* stg = s_stage + (size_t)s * stage_words;
+        for (int u = etid; u < p.R * NG; u += EW * 32) {
+          const int r = u % p.R, g = u / p.R;
+          const uint32_t word = encode_group<C>(stg + r * pitch, s_off, s_thr, g * G, G);
+          const int row_local = st * p.R + r;
+          if constexpr (ENC_ONLY) {
+            const int64_t row = tile * BR + row_local;
+            if (row < p.N) {
+              if constexpr (C >= 8)
+                reinterpret_cast<uint32_t*>(p.codes + row * (C / 2))[g] = word;
+              else if constexpr (C == 4)
+                reinterpret_cast<uint16_t*>(p.codes + row * 2)[0] = (uint16_t)word;
+              else
+                p.codes[row] = (uint8_t)word;
+            }
+          } else {
+            s_codes[(b * BR + row_local) * CBW + g] = word;
+          }
+        }
+        mbar_arrive(&empty[s]);
+      }
+      if constexpr (!ENC_ONLY) mbar_arrive(&cfull[b]);
+    }
+  } else if constexpr (!ENC_ONLY) {
+    // ---------------- scanners ----------------
+    const int stid = tid - 32 * (1 + EW);
+    uint32_t z = 0;
+    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++z) {
+      const int b = z % NB;
+      mbar_wait(&cfull[b], (z / NB) & 1u);
+      const int64_t row = tile * BR + stid;
+      const uint32_t* myc = s_codes + (b * BR + stid) * CBW;
+      uint32_t ae[W], ao[W];
+      scan_core<C, W, U>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
+      mbar_arrive(&cempty[b]);
+      if (row < p.N) store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32);
+    }
+  }
+}
+
+// ------------------------------------------------------------ scan kernel --
+
+template <int C, int W, int U, bool VEC>
+__global__ void __launch_bounds__(256) k_scan_fast(const uint32_t* __restrict__ lut_g,
+                                                   const uint8_t* __restrict__ codes, int64_t N,
+                                                   int M, int32_t* __restrict__ sums,
+                                                   float* __restrict__ out, int64_t ldo, float a,
+                                                   float b, int scale) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
+  for (int i = threadIdx.x; i < C * W * 4; i += blockDim.x)
+    reinterpret_cast<uint4*>(s_lut)[i] = reinterpret_cast<const uint4*>(lut_g)[i];
+  __syncthreads();
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < N;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t* cr = codes + row * ((C + 1) / 2);
+    uint32_t ae[W], ao[W];
+    scan_core<C, W, U>(
+        s_lut,
+        [&](int g) -> uint32_t {
+          if constexpr (C >= 8) return __ldg(reinterpret_cast<const uint32_t*>(cr) + g);
+          else if constexpr (C == 4) return __ldg(reinterpret_cast<const uint16_t*>(cr));
+          else return __ldg(cr);
+        },
+        ae, ao);
+    if (sums) store_sums<W>(sums + row * M, M, scale, ae, ao);
+    if (out) store_row<W, VEC>(out + row * ldo, M, ae, ao, a, b);
+  }
+}
+
+// ------------------------------------------------------------ host side --
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+struct DevInfo {
+  int sms = 148;
+  int smem_optin = 232448;
+};
+
+DevInfo dev_info() {
+  static DevInfo cache[16];
+  static bool have[16] = {};
+  static std::mutex mu;
+  int d = 0;
+  cudaGetDevice(&d);
+  std::lock_guard<std::mutex> g(mu);
+  if (d < 16 && have[d]) return cache[d];
+  DevInfo di;
+  cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, d);
+  cudaDeviceGetAttribute(&di.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+  if (d < 16) {
+    cache[d] = di;
+    have[d] = true;
+  }
+  return di;
+}
+
+struct Geometry {
+  bool ok = false;
+  int SW, nslab, R, NS, slab_words;
+  size_t smem;
+};
+
+// Slab width SW (<= 252 so that a box of SW + 4 columns fits the 256-element
+// TMA box limit) dividing D, then the largest rows-per-stage R (dividing the
+// 256-row tile) that leaves room for >= 4 stages (>= 2 at worst).
+Geometry plan(int C, int W, int D, bool enc_only) {
+  Geometry g;
+  if (D % 4 != 0) return g;
+  int nslab = 0;
+  for (int n = 1; n <= 64; ++n)
+    if (D % n == 0 && (D / n) % 4 == 0 && D / n <= 252) {
+      nslab = n;
+      break;
+    }
+  if (!nslab) return g;
+  g.nslab = nslab;
+  g.SW = D / nslab;
+  const int CBW = C >= 8 ? C / 8 : 1;
+  size_t fixed = BAR_BYTES + 16 * C * 4 + 4 * C * 4 + 16;
+  if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4;
+  fixed = (fixed + 127) & ~size_t(127);
+  const size_t budget = (size_t)dev_info().smem_optin;
+  for (int min_ns : {4, 2}) {
+    for (int R : {256, 128, 64, 32, 16, 8}) {
+      int slab_words = ((R * (g.SW + 4)) + 31) & ~31;
+      size_t stage = (size_t)nslab * slab_words * 4;
+      if (fixed + stage * min_ns > budget) continue;
+      int NS = (int)((budget - fixed) / stage);
+      if (NS > NS_MAX) NS = NS_MAX;
+      g.R = R;
+      g.NS = NS;
+      g.slab_words = slab_words;
+      g.smem = fixed + stage * NS;
+      g.ok = true;
+      return g;
+    }
+  }
+  return g;
+}
+
+bool make_tmap(CUtensorMap* m, const float* A, int64_t N, int64_t lda, int D, int SW, int R) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)N};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
+  cuuint32_t box[2] = {(cuuint32_t)(SW + 4), (cuuint32_t)R};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int C, int W, int U, bool VEC, bool ENC>
+cudaError_t launch_ws_t(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
+  auto k = k_amm_ws<C, W, U, VEC, ENC>;
+  // Per launch: the attribute is per device context and costs ~1 us.
+  cudaError_t attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr_err != cudaSuccess) return attr_err;
+  int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
+  k<<<(unsigned)grid, ENC ? THREADS_ENC : THREADS, smem, s>>>(tm, p);
+  return cudaGetLastError();
+}
+
+template <int C, int W, int U, bool VEC>
+cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int32_t* sums,
+                          float* out, int64_t ldo, cudaStream_t s) {
+  auto k = k_scan_fast<C, W, U, VEC>;
+  size_t smem = (size_t)C * W * 16 * 4;
+  cudaError_t attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr_err != cudaSuccess) return attr_err;
+  int64_t blocks = (N + 255) / 256;
+  int64_t cap = (int64_t)dev_info().sms * (smem > 100000 ? 1 : smem > 60000 ? 2 : 4);
+  if (blocks > cap) blocks = cap;
+  k<<<(unsigned)blocks, 256, smem, s>>>(l.words, codes, N, l.M, sums, out, ldo, l.alpha_eff,
+                                        l.beta32, l.U == 0 ? 1 : l.U);
+  return cudaGetLastError();
+}
+
+// (C, W, U) combinations with compiled fast kernels: every BASELINE config in
+// both modes (U = C for C < 16, else 16), plus common neighbours.
+#define MDN_FAST_COMBOS(X) \
+  X(4, 1, 0) X(4, 1, 4) X(8, 1, 0) X(8, 1, 8) X(8, 2, 0) X(8, 2, 8)                    \
+  X(16, 1, 0) X(16, 1, 16) X(16, 3, 0) X(16, 3, 16) X(16, 4, 0) X(16, 4, 16)            \
+  X(32, 1, 0) X(32, 1, 16) X(32, 3, 0) X(32, 3, 16) X(32, 4, 0) X(32, 4, 16)            \
+  X(32, 25, 0) X(32, 25, 16) X(64, 3, 0) X(64, 3, 16) X(64, 4, 0) X(64, 4, 16)
+
+bool has_combo(int C, int W, int U) {
+#define X(c, w, u) \
+  if (C == c && W == w && U == u) return true;
+  MDN_FAST_COMBOS(X)
+#undef X
+  return false;
+}
+
+bool has_encoder(int C) { return C == 4 || C == 8 || C == 16 || C == 32 || C == 64; }
+
+}  // namespace fast
+
+using namespace fast;
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static bool amm_fast_ok(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
+                        Geometry* geo) {
+  if (!has_combo(t.C, l.W, l.U)) return false;
+  if (!aligned16(A) || lda % 4 != 0) return false;
+  if (!encode_fn()) return false;
+  *geo = plan(t.C, l.W, t.D, false);
+  return geo->ok;
+}
+
+const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
+                             const float* out, int64_t ldo) {
+  Geometry g;
+  if (!amm_fast_ok(t, l, A, lda, &g)) return "generic";
+  const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
+  return vec ? "ws_tma_vec" : "ws_tma";
+}
+
+cudaError_t launch_encode_generic(const TreesDev&, const float*, int64_t, int64_t, uint8_t*,
+                                  cudaStream_t);
+cudaError_t launch_scan_generic(const LutsDev&, const uint8_t*, int64_t, int32_t*, float*, int64_t,
+                                cudaStream_t);
+cudaError_t launch_amm_generic(const TreesDev&, const LutsDev&, const float*, int64_t, int64_t,
+                               float*, int64_t, cudaStream_t);
+
+static Params base_params(const TreesDev& t, const Geometry& g, int64_t N) {
+  Params p{};
+  p.N = N;
+  p.n_tiles = (N + BR - 1) / BR;
+  p.D = t.D;
+  p.SW = g.SW;
+  p.nslab = g.nslab;
+  p.R = g.R;
+  p.NS = g.NS;
+  p.slab_words = g.slab_words;
+  p.dims = t.dims;
+  p.thr = t.thr;
+  return p;
+}
+
+cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int64_t N, int64_t lda,
+                       float* out, int64_t ldo, cudaStream_t s) {
+  Geometry g;
+  if (N > (int64_t)0x7FFFFF00 || !amm_fast_ok(t, l, A, lda, &g))
+    return launch_amm_generic(t, l, A, N, lda, out, ldo, s);
+  CUtensorMap tm;
+  if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R)) return launch_amm_generic(t, l, A, N, lda, out, ldo, s);
+  Params p = base_params(t, g, N);
+  p.ldo = ldo;
+  p.M = l.M;
+  p.alpha_eff = l.alpha_eff;
+  p.beta32 = l.beta32;
+  p.lut = l.words;
+  p.out = out;
+  const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
+#define X(c, w, u)                                                             \
+  if (t.C == c && l.W == w && l.U == u)                                        \
+    return vec ? launch_ws_t<c, w, u, true, false>(tm, p, g.smem, s)           \
+               : launch_ws_t<c, w, u, false, false>(tm, p, g.smem, s);
+  MDN_FAST_COMBOS(X)
+#undef X
+  return launch_amm_generic(t, l, A, N, lda, out, ldo, s);
+}
+
+cudaError_t launch_encode(const TreesDev& t, const float* A, int64_t N, int64_t lda, uint8_t* codes,
+                          cudaStream_t s) {
+  if (N > (int64_t)0x7FFFFF00 || !has_encoder(t.C) || !aligned16(A) || lda % 4 != 0 || !encode_fn())
+    return launch_encode_generic(t, A, N, lda, codes, s);
+  if (t.C >= 8 && (reinterpret_cast<uintptr_t>(codes) & 3u)) return launch_encode_generic(t, A, N, lda, codes, s);
+  if (t.C == 4 && (reinterpret_cast<uintptr_t>(codes) & 1u)) return launch_encode_generic(t, A, N, lda, codes, s);
+  Geometry g = plan(t.C, 1, t.D, true);
+  if (!g.ok) return launch_encode_generic(t, A, N, lda, codes, s);
+  CUtensorMap tm;
+  if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R)) return launch_encode_generic(t, A, N, lda, codes, s);
+  Params p = base_params(t, g, N);
+  p.codes = codes;
+  switch (t.C) {
+    case 4: return launch_ws_t<4, 1, 0, false, true>(tm, p, g.smem, s);
+    case 8: return launch_ws_t<8, 1, 0, false, true>(tm, p, g.smem, s);
+    case 16: return launch_ws_t<16, 1, 0, false, true>(tm, p, g.smem, s);
+    case 32: return launch_ws_t<32, 1, 0, false, true>(tm, p, g.smem, s);
+    case 64: return launch_ws_t<64, 1, 0, false, true>(tm, p, g.smem, s);
+  }
+  return launch_encode_generic(t, A, N, lda, codes, s);
+}
+
+cudaError_t launch_scan(const LutsDev& l, const uint8_t* codes, int64_t N, int32_t* sums,
+                        float* out, int64_t ldo, cudaStream_t s) {
+  const bool codes_ok = l.C >= 8 ? (reinterpret_cast<uintptr_t>(codes) & 3u) == 0
+                                 : (reinterpret_cast<uintptr_t>(codes) & 1u) == 0;
+  if (!has_combo(l.C, l.W, l.U) || !codes_ok) return launch_scan_generic(l, codes, N, sums, out, ldo, s);
+  const bool vec = out && l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
+#define X(c, w, u)                                                                  \
+  if (l.C == c && l.W == w && l.U == u)                                             \
+    return vec ? launch_scan_t<c, w, u, true>(l, codes, N, sums, out, ldo, s)       \
+               : launch_scan_t<c, w, u, false>(l, codes, N, sums, out, ldo, s);
+  MDN_FAST_COMBOS(X)
+#undef X
+  return launch_scan_generic(l, codes, N, sums, out, ldo, s);
+}
+
+}  // namespace mdn
