@@ -28,7 +28,6 @@ sys.path.insert(0, ROOT)
 
 CONFIG = "cls100"
 METRIC = "MADDNESS encode+scan rows/s and % HBM peak (D=512,M=100,C=32), 1/2/4/8 GPUs"
-ROWS_PER_GPU = 1 << 21
 NOMINAL_HBM_GBS = 8000.0
 
 
@@ -114,6 +113,33 @@ def oracle_rows_per_s(A_host: np.ndarray, om, oluts, budget_s: float, mode: str)
     return rows / t_tot, rows, t_tot
 
 
+def _metric(name):
+    if name == CONFIG:
+        return METRIC
+    from datagen.synth import CONFIGS
+    sp = CONFIGS[name]
+    return f"MADDNESS encode+scan rows/s and % HBM peak ({name}: D={sp.D},M={sp.M},C={sp.C})"
+
+
+def _bench_rows(name, rank, ws, device):
+    """This rank's shard of the config's bench-size A (weak scaling)."""
+    from datagen.synth import CHUNK_ROWS, CONFIGS, make_config_data, relu_W, relu_lowrank_torch
+    from paper_2106_10860_b200.dist import shard_rows
+    spec = CONFIGS[name]
+    if spec.kind == "relu":
+        _, n, first_chunk = shard_rows(rank, ws, spec.n_bench, CHUNK_ROWS)
+        return relu_lowrank_torch(relu_W(name), n, first_chunk, device)
+    import torch
+    _, A, _ = make_config_data(name, n_test=spec.n_test, n_train=0)   # 4M patches, tiled
+    reps = spec.n_bench // A.shape[0]
+    return torch.from_numpy(A).to(device).repeat(reps, 1)
+
+
+def _config_B(name):
+    from datagen.synth import CONFIGS, relu_B, sobel_B
+    return relu_B(name) if CONFIGS[name].kind == "relu" else sobel_B(CONFIGS[name].D)
+
+
 def run_reference(args):
     """--impl reference: the oracle timed on the host cores on a bounded sample
     of the same workload (the tier's reference arm)."""
@@ -121,15 +147,17 @@ def run_reference(args):
     if rank != 0:
         return 0
     import oracle as O
-    from datagen.synth import CONFIGS, relu_W, relu_lowrank_torch
-    spec = CONFIGS[CONFIG]
-    blob = open(os.path.join(ROOT, "artifacts", f"{CONFIG}.mdnm"), "rb").read()
+    from datagen.synth import CONFIGS, make_config_data, relu_W, relu_lowrank_torch
+    name = args.config
+    spec = CONFIGS[name]
+    blob = open(os.path.join(ROOT, "artifacts", f"{name}.mdnm"), "rb").read()
     om = O.read_model(blob)
-    from datagen.synth import make_config_data
-    _, _, B = make_config_data(CONFIG, n_test=0)
-    oluts = O.make_luts(om, B, args.mode, spec.U)
+    oluts = O.make_luts(om, _config_B(name), args.mode, spec.U)
     sample = 1 << 16
-    A = relu_lowrank_torch(relu_W(CONFIG), sample, 0, "cpu").numpy()
+    if spec.kind == "relu":
+        A = relu_lowrank_torch(relu_W(name), sample, 0, "cpu").numpy()
+    else:
+        A = make_config_data(name, n_test=sample, n_train=0)[1]
     rows_per_step = ORACLE_CHUNK
     for i in range(args.warmup):
         oracle_step(A[:rows_per_step], om, oluts, args.mode)
@@ -141,12 +169,13 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     value = rows_per_step * len(times) / sum(times)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s",
+        "impl": "reference", "metric": _metric(name), "value": value, "unit": "rows/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "cls100 (D=512, M=100, C=32), " + args.mode + " sum; oracle on "
-                   "16384-row steps from the same generator", "rows_per_step": rows_per_step},
+        "config": {"workload": f"{name} (D={spec.D}, M={spec.M}, C={spec.C}), {args.mode} sum; "
+                   "oracle on 16384-row steps from the same generator",
+                   "rows_per_step": rows_per_step},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": 1, "kind": "oracle",
                          "sample": f"{args.steps} steps x 16384 rows of the bench generator"},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -160,43 +189,51 @@ def run(args):
     import torch.distributed as dist
 
     ws, rank, local = _dist()
+    # MDN_DIST_BACKEND=gloo is a functional check of the multi-rank path on a
+    # single GPU (ranks never wait on each other's kernels); numbers from it
+    # are not bench values. The real path is NCCL, one GPU per rank.
+    backend = os.environ.get("MDN_DIST_BACKEND", "nccl")
     if ws > 1:
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    def allreduce_max(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     dev = torch.cuda.current_device()
     import paper_2106_10860_b200 as mdn
-    from datagen.synth import CHUNK_ROWS, CONFIGS, make_config_data, relu_W, relu_lowrank_torch
+    from datagen.synth import CHUNK_ROWS, CONFIGS, relu_B, relu_W, relu_lowrank_torch
 
-    spec = CONFIGS[CONFIG]
+    name = args.config
+    spec = CONFIGS[name]
     mode = mdn.MDN_SUM_EXACT if args.mode == "exact" else mdn.MDN_SUM_AVG
     # --- model + LUTs: built once on rank 0, broadcast as bytes over NCCL -----
     t_bcast = 0.0
     if rank == 0:
-        model_blob = open(os.path.join(ROOT, "artifacts", f"{CONFIG}.mdnm"), "rb").read()
-        _, _, B = make_config_data(CONFIG, n_test=0)
+        model_blob = open(os.path.join(ROOT, "artifacts", f"{name}.mdnm"), "rb").read()
+        B = _config_B(name)
         m0 = mdn.mdn_model_load(model_blob, dev)
         l0 = mdn.mdn_build_luts(m0, B, mode, spec.U)
         luts_blob = mdn.mdn_luts_serialize(l0)
     if ws > 1:
+        from paper_2106_10860_b200.dist import broadcast_blobs
         t0 = time.perf_counter()
-        sizes = torch.zeros(2, dtype=torch.int64, device="cuda")
-        if rank == 0:
-            sizes[0], sizes[1] = len(model_blob), len(luts_blob)
-        dist.broadcast(sizes, 0)
-        buf = torch.empty(int(sizes[0] + sizes[1]), dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            buf.copy_(torch.frombuffer(bytearray(model_blob + luts_blob), dtype=torch.uint8))
-        dist.broadcast(buf, 0)
-        host = buf.cpu().numpy().tobytes()
-        model_blob, luts_blob = host[:int(sizes[0])], host[int(sizes[0]):]
+        model_blob, luts_blob = broadcast_blobs([model_blob, luts_blob] if rank == 0 else None, 0)
         t_bcast = time.perf_counter() - t0
     model = mdn.mdn_model_load(model_blob, dev)
     luts = mdn.mdn_luts_load(luts_blob, dev)
 
     # --- this rank's shard of A (2^21 rows, chunks rank*2 .. rank*2+1) --------
-    n = ROWS_PER_GPU
-    first_chunk = rank * (n // CHUNK_ROWS)
-    A = relu_lowrank_torch(relu_W(CONFIG), n, first_chunk, "cuda")
+    A = _bench_rows(name, rank, ws, "cuda")
+    n = A.shape[0]
     out = torch.empty((n, spec.M), dtype=torch.float32, device="cuda")
     stream = torch.cuda.Stream()
     torch.cuda.synchronize()
@@ -223,10 +260,7 @@ def run(args):
     per_launch = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     elapsed_ms = ev[0].elapsed_time(ev[-1])
     clocks = _clock_summary(clk)
-    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
-    if ws > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t_max.item())
+    elapsed_ms = allreduce_max(elapsed_ms)
 
     rows_total = n * ws * args.steps
     value = rows_total / (elapsed_ms / 1e3)
@@ -239,7 +273,7 @@ def run(args):
     nmse = None
     cublas = None
     if rank == 0:
-        _, _, B = make_config_data(CONFIG, n_test=0)
+        B = _config_B(name)
         Bd = torch.from_numpy(B).cuda()
         rows = 65536
         exact = (A[:rows].double() @ Bd.double())
@@ -260,9 +294,11 @@ def run(args):
     # --- e2e: the same metric through the public API with HOST buffers --------
     e2e = None
     if rank == 0 or ws > 1:
-        ex = mdn.mdn_exec_create(model, luts, chunk_rows=1 << 17, n_slots=3)
-        A_h = A.cpu().pin_memory()
-        out_h = torch.empty((n, spec.M), dtype=torch.float32).pin_memory()
+        ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
+                                 n_slots=3)
+        n_e2e = min(n, (1 << 32) // (4 * spec.D))     # <= 4 GiB of pinned host A per rank
+        A_h = A[:n_e2e].cpu().pin_memory()
+        out_h = torch.empty((n_e2e, spec.M), dtype=torch.float32).pin_memory()
         mdn.mdn_amm_host(ex, A_h, out_h)                      # warm-up
         e2e_steps = max(1, min(args.steps, 3))
         if ws > 1:
@@ -270,11 +306,11 @@ def run(args):
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             mdn.mdn_amm_host(ex, A_h, out_h)                  # synchronous: H2D + kernel + D2H
-        t_e2e = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-        if ws > 1:
-            dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-        e2e = {"value": n * ws * e2e_steps / float(t_e2e.item()), "unit": "rows/s",
-               "h2d_bytes_per_step": n * 4 * spec.D * ws, "d2h_bytes_per_step": n * 4 * spec.M * ws,
+        t_e2e = allreduce_max(time.perf_counter() - t0)
+        e2e = {"value": n_e2e * ws * e2e_steps / t_e2e, "unit": "rows/s",
+               "rows_per_step": n_e2e * ws,
+               "h2d_bytes_per_step": n_e2e * 4 * spec.D * ws,
+               "d2h_bytes_per_step": n_e2e * 4 * spec.M * ws,
                "steps": e2e_steps, "path": "mdn_amm_host (pinned host A -> 3-slot pipelined "
                "H2D/kernel/D2H)"}
         ex.close()
@@ -297,20 +333,21 @@ def run(args):
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(f"{CONFIG}_{args.mode}")
+                traffic = json.load(open(tp)).get(f"{name}_{args.mode}")
             except Exception:
                 traffic = None
         line = {
-            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": ws,
+            "metric": _metric(name), "value": value, "unit": "rows/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
-            "config": {"workload": f"cls100: D=512, M=100, C=32, K=16, {args.mode} sum"
+            "config": {"workload": f"{name}: D={spec.D}, M={spec.M}, C={spec.C}, K=16, {args.mode} sum"
                        + (f" (U={spec.U})" if args.mode == "avg" else "")
-                       + "; relu rank-64 rows, oracle-trained trees/ridge prototypes",
+                       + ("; relu low-rank rows" if spec.kind == "relu" else "; 3x3x3 image patches")
+                       + ", oracle-trained trees / ridge prototypes",
                        "rows_per_gpu": n, "global_rows_per_step": n * ws,
                        "A_bytes_per_gpu": n * 4 * spec.D,
-                       "l2": "inputs 4 GiB per GPU > 126 MB L2; no flush",
+                       "l2": f"inputs {n * 4 * spec.D / 2**30:.1f} GiB per GPU > 126 MB L2; no flush",
                        "parallelism": f"row-sharded dp{ws}, model+LUT NCCL broadcast once"},
             "pct_hbm_nominal_8tbs": achieved_gbs / NOMINAL_HBM_GBS,
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
@@ -340,6 +377,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--mode", choices=["exact", "avg"], default="exact")
+    ap.add_argument("--config", default=CONFIG,
+                    help="workload (default: the headline cls100 config); others for DESIGN.md tables")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

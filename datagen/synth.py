@@ -13,7 +13,8 @@ Recipe (DESIGN.md "Input recipe"):
   L837), standing in for Caltech101.
 
 Host draws use numpy PCG64 ``default_rng(seed)`` in float64, cast to float32
-once at the end, in the fixed order W, train (Z, eps), test (Z, eps), B.
+once at the end, in the fixed order W, train (Z, eps), test (Z, eps); B has its
+own stream ``default_rng([seed, 0xB])``.
 Bench-size A (larger than the 126 MB L2) is generated with torch in 2^20-row
 chunks, chunk q seeded ``1000 + q`` (draw Z then eps), W taken from the host
 draw; global row r therefore does not depend on how rows are sharded.
@@ -84,8 +85,15 @@ def _relu_host(spec: ConfigSpec, n_test: int | None):
     A_train = _relu_rows(rng, spec.n_train, W)
     nt = spec.n_test if n_test is None else n_test
     A_test = _relu_rows(rng, nt, W) if nt > 0 else np.zeros((0, spec.D), np.float32)
-    B = (rng.standard_normal((spec.D, spec.M)) / np.sqrt(spec.D)).astype(np.float32)
-    return A_train, A_test, B, W.astype(np.float32)
+    return A_train, A_test, relu_B(spec.name), W.astype(np.float32)
+
+
+def relu_B(name: str) -> np.ndarray:
+    """B ~ N(0, 1/D)^{D x M} from its own stream (seed [seed, 0xB]), so B does
+    not depend on how many train/test rows were drawn."""
+    spec = CONFIGS[name]
+    rng = np.random.default_rng([spec.seed, 0xB])
+    return (rng.standard_normal((spec.D, spec.M)) / np.sqrt(spec.D)).astype(np.float32)
 
 
 # ----------------------------------------------------------------------------
@@ -185,7 +193,8 @@ def relu_W(name: str) -> np.ndarray:
     return rng.standard_normal((spec.rank, spec.D)).astype(np.float32)
 
 
-def relu_lowrank_torch(W, n_rows: int, first_chunk: int, device, out=None, noise: float = 0.1):
+def relu_lowrank_torch(W, n_rows: int, first_chunk: int, device, out=None, noise: float = 0.1,
+                       chunk_rows: int = CHUNK_ROWS):
     """Bench-size relu rows generated with torch in 2^20-row chunks.
 
     Rows [q*2^20, (q+1)*2^20) of the global bench matrix come from chunk q
@@ -200,11 +209,11 @@ def relu_lowrank_torch(W, n_rows: int, first_chunk: int, device, out=None, noise
         out = torch.empty((n_rows, D), dtype=torch.float32, device=device)
     done, q = 0, first_chunk
     while done < n_rows:
-        take = min(CHUNK_ROWS, n_rows - done)
+        take = min(chunk_rows, n_rows - done)
         g = torch.Generator(device=device)
         g.manual_seed(CHUNK_SEED_BASE + q)
-        z = torch.randn((CHUNK_ROWS, r), generator=g, device=device, dtype=torch.float32)
-        eps = torch.randn((CHUNK_ROWS, D), generator=g, device=device, dtype=torch.float32)
+        z = torch.randn((chunk_rows, r), generator=g, device=device, dtype=torch.float32)
+        eps = torch.randn((chunk_rows, D), generator=g, device=device, dtype=torch.float32)
         blk = torch.addmm(eps[:take].mul_(noise), z[:take], W)
         out[done:done + take] = blk.clamp_min_(0.0)
         done += take
