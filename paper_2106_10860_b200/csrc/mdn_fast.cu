@@ -36,15 +36,23 @@
 namespace mdn {
 namespace fast {
 
-constexpr int E_WARPS = 2;               // encoder warps (fused kernel)
-constexpr int S_WARPS = 8;               // scanner warps
-constexpr int BR = S_WARPS * 32;         // rows per tile
+constexpr int BR = 256;                  // rows per tile
 constexpr int NB = 3;                    // code ring depth (tiles)
 constexpr int NS_MAX = 8;                // A stage ring depth cap
-constexpr int THREADS = 32 * (1 + E_WARPS + S_WARPS);
-constexpr int E_WARPS_ENC = 8;           // encoder warps (encode-only kernel)
-constexpr int THREADS_ENC = 32 * (1 + E_WARPS_ENC);
 constexpr int BAR_BYTES = 256;
+
+// Warp roles. Per row an encoder spends ~25 instructions per codebook
+// (4 split-dim loads, 4 threshold gathers, compares), a scanner ~4W per
+// codebook (W table words of 4 columns), so the encoder:scanner split follows
+// 25 : 4W -- 2:8 for the 100-column tables, 6:4 for 10-16 columns, 8:2 for
+// <= 8 columns (ncu on the image config: scanners idle 63% at 2:8).
+template <int W, bool ENC_ONLY>
+struct Roles {
+  static constexpr int E = ENC_ONLY ? 8 : (W >= 8 ? 2 : (W >= 3 ? 6 : 8));
+  static constexpr int S = ENC_ONLY ? 0 : (W >= 8 ? 8 : (W >= 3 ? 4 : 2));
+  static constexpr int THREADS = 32 * (1 + E + S);
+  static constexpr int ROWS_PER_SCANNER = ENC_ONLY ? 0 : BR / (32 * S);
+};
 
 struct Params {
   int64_t N;
@@ -56,6 +64,7 @@ struct Params {
   float alpha_eff, beta32;
   const uint32_t* lut;            // global [C][W][16]
   const uint16_t* dims;           // global [C][4]
+  const uint16_t* sub;            // global [C] subspace begin
   const float* thr;               // global [C][16]
   float* out;
   uint8_t* codes;                 // encode-only output
@@ -203,16 +212,44 @@ __device__ __forceinline__ void store_sums(int32_t* __restrict__ o, int M, int s
 
 // ------------------------------------------------------------ fused kernel --
 
-template <int C>
+__device__ __forceinline__ float pick4(const float4& v, int s) {
+  const float a = (s & 1) ? v.y : v.x;
+  const float b = (s & 1) ? v.w : v.z;
+  return (s & 2) ? b : a;
+}
+
+// SUBF = 0: the 4 split-dim values are read one by one (s_off: word offsets).
+// SUBF = 1 / 2: the codebook's whole subspace (<= 4 / <= 8 columns, 16-B
+// aligned) is read with 1 / 2 conflict-free LDS.128 (row pitch == 4 mod 32
+// words) and the split dims picked with warp-uniform selects (s_off: column
+// within the subspace, s_base: subspace word offset) -- 4x / 2x fewer shared
+// wavefronts than four 4-way-conflicted LDS.32.
+template <int C, int SUBF>
 __device__ __forceinline__ uint32_t encode_group(const float* __restrict__ rowp,
                                                  const int* __restrict__ s_off,
-                                                 const float* __restrict__ s_thr, int c0, int G) {
+                                                 const int* __restrict__ s_base,
+                                                 const float* __restrict__ s_thr, int c0) {
   uint32_t word = 0;
 #pragma unroll
   for (int i = 0; i < (C >= 8 ? 8 : C); ++i) {
     const int c = c0 + i;
     const int4 o = *reinterpret_cast<const int4*>(s_off + 4 * c);
-    const float x0 = rowp[o.x], x1 = rowp[o.y], x2 = rowp[o.z], x3 = rowp[o.w];
+    float x0, x1, x2, x3;
+    if constexpr (SUBF == 0) {
+      x0 = rowp[o.x], x1 = rowp[o.y], x2 = rowp[o.z], x3 = rowp[o.w];
+    } else {
+      const float4* vb = reinterpret_cast<const float4*>(rowp + s_base[c]);
+      const float4 v0 = vb[0];
+      if constexpr (SUBF == 1) {
+        x0 = pick4(v0, o.x), x1 = pick4(v0, o.y), x2 = pick4(v0, o.z), x3 = pick4(v0, o.w);
+      } else {
+        const float4 v1 = vb[1];
+        x0 = (o.x & 4) ? pick4(v1, o.x) : pick4(v0, o.x);
+        x1 = (o.y & 4) ? pick4(v1, o.y) : pick4(v0, o.y);
+        x2 = (o.z & 4) ? pick4(v1, o.z) : pick4(v0, o.z);
+        x3 = (o.w & 4) ? pick4(v1, o.w) : pick4(v0, o.w);
+      }
+    }
     const float* th = s_thr + 16 * c;
     // Algorithm 1: i <- 2i - 1 + [x_{j^t} >= v^t_i]  (0-based: p <- 2p + b)
     uint32_t p = x0 >= th[0] ? 1u : 0u;
@@ -224,13 +261,15 @@ __device__ __forceinline__ uint32_t encode_group(const float* __restrict__ rowp,
   return word;
 }
 
-template <int C, int W, int U, bool VEC, bool ENC_ONLY>
-__global__ void __launch_bounds__(ENC_ONLY ? THREADS_ENC : THREADS, 1)
+template <int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF>
+__global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
     k_amm_ws(const __grid_constant__ CUtensorMap tmap, const Params p) {
   constexpr int G = C >= 8 ? 8 : C;      // codebooks per encoder unit (one code word)
   constexpr int NG = C / G;
   constexpr int CBW = NG;                // code words per row
-  constexpr int EW = ENC_ONLY ? E_WARPS_ENC : E_WARPS;
+  constexpr int EW = Roles<W, ENC_ONLY>::E;
+  constexpr int SWN = Roles<W, ENC_ONLY>::S;
+  constexpr int KR = Roles<W, ENC_ONLY>::ROWS_PER_SCANNER;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NS_MAX;
@@ -240,11 +279,13 @@ __global__ void __launch_bounds__(ENC_ONLY ? THREADS_ENC : THREADS, 1)
   // the shared window (plain LDS/STS, no generic loads).
   constexpr int OFF_THR = BAR_BYTES;
   constexpr int OFF_OFF = OFF_THR + 16 * C * 4;
-  constexpr int OFF_LUT = (OFF_OFF + 4 * C * 4 + 15) & ~15;
+  constexpr int OFF_BASE = OFF_OFF + 4 * C * 4;
+  constexpr int OFF_LUT = (OFF_BASE + C * 4 + 15) & ~15;
   constexpr int OFF_CODES = OFF_LUT + (ENC_ONLY ? 0 : C * W * 16 * 4);
   constexpr int OFF_STAGE = (OFF_CODES + (ENC_ONLY ? 0 : NB * BR * CBW * 4) + 127) & ~127;
   float* s_thr = reinterpret_cast<float*>(smem + OFF_THR);
   int* s_off = reinterpret_cast<int*>(smem + OFF_OFF);
+  int* s_base = reinterpret_cast<int*>(smem + OFF_BASE);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
   uint32_t* s_codes = reinterpret_cast<uint32_t*>(smem + OFF_CODES);
   float* s_stage = reinterpret_cast<float*>(smem + OFF_STAGE);
@@ -256,7 +297,11 @@ __global__ void __launch_bounds__(ENC_ONLY ? THREADS_ENC : THREADS, 1)
   for (int i = tid; i < 16 * C; i += blockDim.x) s_thr[i] = p.thr[i];
   for (int i = tid; i < 4 * C; i += blockDim.x) {
     const int d = p.dims[i];
-    s_off[i] = (d / p.SW) * p.slab_words + (d % p.SW);
+    s_off[i] = SUBF ? d - p.sub[i / 4] : (d / p.SW) * p.slab_words + (d % p.SW);
+  }
+  for (int c = tid; c < C; c += blockDim.x) {
+    const int b = p.sub[c];
+    s_base[c] = (b / p.SW) * p.slab_words + (b % p.SW);
   }
   if constexpr (!ENC_ONLY) {
     const uint4* src = reinterpret_cast<const uint4*>(p.lut);
@@ -270,7 +315,7 @@ __global__ void __launch_bounds__(ENC_ONLY ? THREADS_ENC : THREADS, 1)
     }
     for (int b = 0; b < NB; ++b) {
       mbar_init(&cfull[b], EW * 32);
-      mbar_init(&cempty[b], S_WARPS * 32);
+      mbar_init(&cempty[b], SWN > 0 ? SWN * 32 : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -313,7 +358,7 @@ __global__ void __launch_bounds__(ENC_ONLY ? THREADS_ENC : THREADS, 1)
         const float* stg = s_stage + (size_t)s * stage_words;
         for (int u = etid; u < p.R * NG; u += EW * 32) {
           const int r = u % p.R, g = u / p.R;
-          const uint32_t word = encode_group<C>(stg + r * pitch, s_off, s_thr, g * G, G);
+          const uint32_t word = encode_group<C, SUBF>(stg + r * pitch, s_off, s_base, s_thr, g * G);
           const int row_local = st * p.R + r;
           if constexpr (ENC_ONLY) {
             const int64_t row = tile * BR + row_local;
@@ -340,12 +385,16 @@ __global__ void __launch_bounds__(ENC_ONLY ? THREADS_ENC : THREADS, 1)
     for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++z) {
       const int b = z % NB;
       mbar_wait(&cfull[b], (z / NB) & 1u);
-      const int64_t row = tile * BR + stid;
-      const uint32_t* myc = s_codes + (b * BR + stid) * CBW;
-      uint32_t ae[W], ao[W];
-      scan_core<C, W, U>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
-      mbar_arrive(&cempty[b]);
-      if (row < p.N) store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32);
+#pragma unroll 1
+      for (int k = 0; k < KR; ++k) {
+        const int rl = stid + k * SWN * 32;
+        const int64_t row = tile * BR + rl;
+        const uint32_t* myc = s_codes + (b * BR + rl) * CBW;
+        uint32_t ae[W], ao[W];
+        scan_core<C, W, U>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
+        if (k == KR - 1) mbar_arrive(&cempty[b]);
+        if (row < p.N) store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32);
+      }
     }
   }
 }
@@ -446,7 +495,7 @@ Geometry plan(int C, int W, int D, bool enc_only) {
   g.nslab = nslab;
   g.SW = D / nslab;
   const int CBW = C >= 8 ? C / 8 : 1;
-  size_t fixed = BAR_BYTES + 16 * C * 4 + 4 * C * 4 + 16;
+  size_t fixed = BAR_BYTES + 16 * C * 4 + 4 * C * 4 + C * 4 + 16;
   if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4;
   fixed = (fixed + 127) & ~size_t(127);
   const size_t budget = (size_t)dev_info().smem_optin;
@@ -480,15 +529,26 @@ bool make_tmap(CUtensorMap* m, const float* A, int64_t N, int64_t lda, int D, in
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int C, int W, int U, bool VEC, bool ENC>
-cudaError_t launch_ws_t(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
-  auto k = k_amm_ws<C, W, U, VEC, ENC>;
+template <int C, int W, int U, bool VEC, bool ENC, int SUBF>
+cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
+  auto k = k_amm_ws<C, W, U, VEC, ENC, SUBF>;
   // Per launch: the attribute is per device context and costs ~1 us.
   cudaError_t attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr_err != cudaSuccess) return attr_err;
   int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
-  k<<<(unsigned)grid, ENC ? THREADS_ENC : THREADS, smem, s>>>(tm, p);
+  k<<<(unsigned)grid, Roles<W, ENC>::THREADS, smem, s>>>(tm, p);
   return cudaGetLastError();
+}
+
+// Subspace-vector encoders are compiled for the small-D tables (C <= 8).
+template <int C, int W, int U, bool VEC, bool ENC>
+cudaError_t launch_ws_t(const CUtensorMap& tm, const Params& p, int subf, size_t smem,
+                        cudaStream_t s) {
+  if constexpr (C <= 8) {
+    if (subf == 1) return launch_ws_sf<C, W, U, VEC, ENC, 1>(tm, p, smem, s);
+    if (subf == 2) return launch_ws_sf<C, W, U, VEC, ENC, 2>(tm, p, smem, s);
+  }
+  return launch_ws_sf<C, W, U, VEC, ENC, 0>(tm, p, smem, s);
 }
 
 template <int C, int W, int U, bool VEC>
@@ -544,7 +604,10 @@ const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A
   Geometry g;
   if (!amm_fast_ok(t, l, A, lda, &g)) return "generic";
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
-  return vec ? "ws_tma_vec" : "ws_tma";
+  const int sf = g.nslab == 1 ? t.subf : 0;
+  static const char* names[2][3] = {{"ws_tma", "ws_tma_sub4", "ws_tma_sub8"},
+                                    {"ws_tma_vec", "ws_tma_vec_sub4", "ws_tma_vec_sub8"}};
+  return names[vec][sf];
 }
 
 cudaError_t launch_encode_generic(const TreesDev&, const float*, int64_t, int64_t, uint8_t*,
@@ -565,6 +628,7 @@ static Params base_params(const TreesDev& t, const Geometry& g, int64_t N) {
   p.NS = g.NS;
   p.slab_words = g.slab_words;
   p.dims = t.dims;
+  p.sub = t.sub;
   p.thr = t.thr;
   return p;
 }
@@ -577,6 +641,7 @@ cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int6
   CUtensorMap tm;
   if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R)) return launch_amm_generic(t, l, A, N, lda, out, ldo, s);
   Params p = base_params(t, g, N);
+  const int sf = g.nslab == 1 ? t.subf : 0;   // subspace loads stay inside one slab
   p.ldo = ldo;
   p.M = l.M;
   p.alpha_eff = l.alpha_eff;
@@ -586,8 +651,8 @@ cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int6
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
 #define X(c, w, u)                                                             \
   if (t.C == c && l.W == w && l.U == u)                                        \
-    return vec ? launch_ws_t<c, w, u, true, false>(tm, p, g.smem, s)           \
-               : launch_ws_t<c, w, u, false, false>(tm, p, g.smem, s);
+    return vec ? launch_ws_t<c, w, u, true, false>(tm, p, sf, g.smem, s)       \
+               : launch_ws_t<c, w, u, false, false>(tm, p, sf, g.smem, s);
   MDN_FAST_COMBOS(X)
 #undef X
   return launch_amm_generic(t, l, A, N, lda, out, ldo, s);
@@ -604,13 +669,14 @@ cudaError_t launch_encode(const TreesDev& t, const float* A, int64_t N, int64_t 
   CUtensorMap tm;
   if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R)) return launch_encode_generic(t, A, N, lda, codes, s);
   Params p = base_params(t, g, N);
+  const int sf = g.nslab == 1 ? t.subf : 0;
   p.codes = codes;
   switch (t.C) {
-    case 4: return launch_ws_t<4, 1, 0, false, true>(tm, p, g.smem, s);
-    case 8: return launch_ws_t<8, 1, 0, false, true>(tm, p, g.smem, s);
-    case 16: return launch_ws_t<16, 1, 0, false, true>(tm, p, g.smem, s);
-    case 32: return launch_ws_t<32, 1, 0, false, true>(tm, p, g.smem, s);
-    case 64: return launch_ws_t<64, 1, 0, false, true>(tm, p, g.smem, s);
+    case 4: return launch_ws_t<4, 1, 0, false, true>(tm, p, sf, g.smem, s);
+    case 8: return launch_ws_t<8, 1, 0, false, true>(tm, p, sf, g.smem, s);
+    case 16: return launch_ws_t<16, 1, 0, false, true>(tm, p, sf, g.smem, s);
+    case 32: return launch_ws_t<32, 1, 0, false, true>(tm, p, sf, g.smem, s);
+    case 64: return launch_ws_t<64, 1, 0, false, true>(tm, p, sf, g.smem, s);
   }
   return launch_encode_generic(t, A, N, lda, codes, s);
 }

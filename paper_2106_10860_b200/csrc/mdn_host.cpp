@@ -125,6 +125,7 @@ void mdn_model_free(mdn_model* m) {
     cudaFree(m->d_dims);
     cudaFree(m->d_thr);
     cudaFree(m->d_P);
+    cudaFree(m->d_sub);
   }
   delete m;
 }
@@ -152,16 +153,27 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   m->seed = r.get<uint64_t>();
   m->h_dims.assign((size_t)C * 4, 0);
   m->h_thr.assign((size_t)C * THR_STRIDE, 0.f);
+  m->h_sub.assign(C, 0);
+  int max_w = 0;
+  bool aligned = true;
   for (uint32_t c = 0; c < C; ++c) {
     size_t rec = r.off;
     uint32_t b = r.get<uint32_t>(), e = r.get<uint32_t>();
+    m->h_sub[c] = (uint16_t)b;
+    if ((int)(e - b) > max_w) max_w = (int)(e - b);
+    if (b % 4) aligned = false;
     for (int t = 0; t < 4; ++t) m->h_dims[c * 4 + t] = r.get<uint16_t>();
     for (int i = 0; i < 15; ++i) m->h_thr[c * THR_STRIDE + i] = r.get<float>();
     if (r.fail) return set_err(err_off, r.fail_off, MDN_EFORMAT);
     if (b > e || e > D) return set_err(err_off, rec, MDN_EFORMAT);
-    for (int t = 0; t < 4; ++t)
+    for (int t = 0; t < 4; ++t) {
       if (m->h_dims[c * 4 + t] >= D) return set_err(err_off, rec + 8 + 2 * t, MDN_EINVAL);
+      // split dims must lie in the codebook's subspace (reading R2)
+      if (m->h_dims[c * 4 + t] < b || m->h_dims[c * 4 + t] >= e)
+        return set_err(err_off, rec + 8 + 2 * t, MDN_EFORMAT);
+    }
   }
+  m->subf = aligned && max_w <= 4 ? 1 : (aligned && max_w <= 8 ? 2 : 0);
   size_t p_bytes = (size_t)K * C * D * sizeof(float);
   if (!r.need(p_bytes + 8)) return set_err(err_off, r.fail_off, MDN_EFORMAT);
   const uint8_t* P = r.p + r.off;
@@ -179,14 +191,16 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
     mdn_model_free(m.release());
     return st;
   }
-  if ((st = dalloc(&m->d_P, (size_t)K * C * D)) != MDN_OK) {
+  if ((st = dalloc(&m->d_P, (size_t)K * C * D)) != MDN_OK ||
+      (st = dalloc(&m->d_sub, (size_t)C)) != MDN_OK) {
     mdn_model_free(m.release());
     return st;
   }
   cudaError_t e1 = cudaMemcpy(m->d_dims, m->h_dims.data(), m->h_dims.size() * 2, cudaMemcpyHostToDevice);
   cudaError_t e2 = cudaMemcpy(m->d_thr, m->h_thr.data(), m->h_thr.size() * 4, cudaMemcpyHostToDevice);
   cudaError_t e3 = cudaMemcpy(m->d_P, P, p_bytes, cudaMemcpyHostToDevice);
-  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+  cudaError_t e4 = cudaMemcpy(m->d_sub, m->h_sub.data(), C * 2, cudaMemcpyHostToDevice);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
     mdn_model_free(m.release());
     return MDN_ECUDA;
   }

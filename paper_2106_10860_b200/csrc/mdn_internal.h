@@ -20,8 +20,10 @@ constexpr int MAX_C = 256;         // S <= 255 * C must fit the 16-bit SWAR lane
 struct TreesDev {
   const uint16_t* dims;  // [C][4] global column of each level's split
   const float* thr;      // [C][16] heap order, pad slot 15 unused
+  const uint16_t* sub;   // [C] first column of each codebook's subspace J^(c)
   int C;
   int D;
+  int subf;              // 1 / 2: every subspace is 16-B aligned and <= 4 / 8 wide
 };
 
 // Quantised tables as the kernels consume them (device).
@@ -69,10 +71,13 @@ struct mdn_model {
   uint64_t n_train, seed, fingerprint;
   std::vector<uint16_t> h_dims;   // [C][4]
   std::vector<float> h_thr;       // [C][16]
+  std::vector<uint16_t> h_sub;    // [C] subspace begin
+  int subf = 0;
   uint16_t* d_dims = nullptr;
   float* d_thr = nullptr;
+  uint16_t* d_sub = nullptr;
   float* d_P = nullptr;           // [16C][D]
-  mdn::TreesDev trees() const { return {d_dims, d_thr, C, D}; }
+  mdn::TreesDev trees() const { return {d_dims, d_thr, d_sub, C, D, subf}; }
 };
 
 struct mdn_luts {
