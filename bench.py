@@ -238,8 +238,20 @@ def run(args):
     stream = torch.cuda.Stream()
     torch.cuda.synchronize()
 
+    op = args.op
+    codes = None
+    if op != "amm":
+        codes = torch.empty((n, (spec.C + 1) // 2), dtype=torch.uint8, device="cuda")
+        mdn.mdn_encode(model, A, codes)
+        torch.cuda.synchronize()
+
     def step():
-        mdn.mdn_amm(model, luts, A, out, stream=stream)
+        if op == "amm":
+            mdn.mdn_amm(model, luts, A, out, stream=stream)
+        elif op == "encode":
+            mdn.mdn_encode(model, A, codes, stream=stream)
+        else:
+            mdn.mdn_scan(luts, codes, out=out, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -264,7 +276,25 @@ def run(args):
 
     rows_total = n * ws * args.steps
     value = rows_total / (elapsed_ms / 1e3)
-    bytes_per_row = 4 * spec.D + 4 * spec.M
+    bytes_per_row = {"amm": 4 * spec.D + 4 * spec.M, "encode": 4 * spec.D + (spec.C + 1) // 2,
+                     "scan": (spec.C + 1) // 2 + 4 * spec.M}[op]
+
+    # Achievable-bandwidth probe: a plain streaming kernel with the same byte
+    # mix (read A, write M floats per row), timed the same way.
+    probe = None
+    if op == "amm" and spec.D % 4 == 0:
+        for _ in range(2):
+            mdn.mdn_stream_probe(A, out, stream=stream)
+        pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize()
+        pe[0].record(stream)
+        for _ in range(args.steps):
+            mdn.mdn_stream_probe(A, out, stream=stream)
+        pe[1].record(stream)
+        torch.cuda.synchronize()
+        t_probe = pe[0].elapsed_time(pe[1]) / 1e3 / args.steps
+        probe = {"gbs": n * bytes_per_row / t_probe / 1e9,
+                 "what": "plain streaming kernel, same bytes (read A, write M floats/row), no tables"}
     peak, peak_kind = _peaks()
     avg_launch_s = statistics.mean(per_launch) / 1e3
     achieved_gbs = n * bytes_per_row / avg_launch_s / 1e9
@@ -272,7 +302,7 @@ def run(args):
     # --- quality (NMSE vs exact fp64 AB on 65536 rows) and the cuBLAS context point
     nmse = None
     cublas = None
-    if rank == 0:
+    if rank == 0 and op == "amm":
         B = _config_B(name)
         Bd = torch.from_numpy(B).cuda()
         rows = 65536
@@ -293,7 +323,7 @@ def run(args):
 
     # --- e2e: the same metric through the public API with HOST buffers --------
     e2e = None
-    if rank == 0 or ws > 1:
+    if op == "amm" and (rank == 0 or ws > 1):
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
                                  n_slots=3)
         n_e2e = min(n, (1 << 32) // (4 * spec.D))     # <= 4 GiB of pinned host A per rank
@@ -318,7 +348,7 @@ def run(args):
 
     # --- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only ---
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and op == "amm":
         import oracle as O
         om = O.read_model(model_blob)
         oluts = O.make_luts(om, B, args.mode, spec.U)
@@ -337,7 +367,8 @@ def run(args):
             except Exception:
                 traffic = None
         line = {
-            "metric": _metric(name), "value": value, "unit": "rows/s", "n_gpus": ws,
+            "metric": _metric(name) + ("" if op == "amm" else f" [{op} only]"), "value": value,
+            "unit": "rows/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
@@ -354,10 +385,13 @@ def run(args):
                          "frac": achieved_gbs / peak, "peak_kind": peak_kind,
                          "traffic": traffic,
                          "algorithmic_bytes_per_launch": n * bytes_per_row,
-                         "kernel": mdn.mdn_amm_variant(model, luts, spec.D)},
+                         "kernel": mdn.mdn_amm_variant(model, luts, spec.D) if op == "amm" else op,
+                         "frac_of_stream_probe": (achieved_gbs / probe["gbs"]) if probe else None},
+            "stream_probe": probe,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,
+            "op": op,
             "clocks": clocks,
             "nmse_vs_exact_fp64": nmse,
             "context": {"cublas_fp32_rows_per_s": cublas,
@@ -380,6 +414,8 @@ def main():
     ap.add_argument("--config", default=CONFIG,
                     help="workload (default: the headline cls100 config); others for DESIGN.md tables")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--op", choices=["amm", "encode", "scan"], default="amm",
+                    help="amm (the hot path, default) or the unfused halves, for DESIGN.md")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -152,6 +152,16 @@ void mdn_exec_free(mdn_exec* exec);
 int mdn_amm_host(mdn_exec* exec, const float* A_host, int64_t N, int64_t lda,
                  float* out_host, int64_t ldo);
 
+/* --------------------------------------------------------- diagnostics -- */
+
+/* Roofline probe (not part of the method): a plain streaming kernel with the
+ * fused path's byte mix -- reads every element of A (device fp32 N x D, lda,
+ * D % 4 == 0, 16-B aligned) and writes M floats per row of out (device,
+ * ldo) -- so bench.py can report the achievable bandwidth for this mix next
+ * to the fused kernel's. */
+int mdn_stream_probe(const float* A, int64_t N, int64_t lda, int64_t D, float* out,
+                     int64_t ldo, int64_t M, void* stream);
+
 /* --------------------------------------------------------------- misc -- */
 
 const char* mdn_status_str(int status);

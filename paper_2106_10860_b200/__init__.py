@@ -26,7 +26,7 @@ K = 16
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"libmaddness.so not built at {LIB_PATH}; run `python -m paper_2106_10860_b200.build` "
+        f"libmaddness.so not built at {LIB_PATH}; run `python paper_2106_10860_b200/build.py` "
         "(there is no CPU fallback)")
 
 _lib = ct.CDLL(LIB_PATH)
@@ -52,6 +52,7 @@ _SIGS = {
     "mdn_status_str": (ct.c_char_p, [_i32]),
     "mdn_abi_version": (_i32, []),
     "mdn_amm_variant": (_i32, [_vp, _vp, _i64, ct.c_char_p, _sz]),
+    "mdn_stream_probe": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -251,6 +252,15 @@ def mdn_amm_host(ex: Exec, A_host, out_host):
         raise ValueError("row count mismatch")
     _check(_lib.mdn_amm_host(ex._h, pa, sa[0], lda, po, ldo), "mdn_amm_host")
     return out_host
+
+
+def mdn_stream_probe(A, out, stream=None):
+    """Diagnostics: stream A (read) and out (write) with the fused path's byte mix."""
+    pa = _dev_ptr(A, "float32", "A")
+    po = _dev_ptr(out, "float32", "out")
+    _check(_lib.mdn_stream_probe(pa, A.shape[0], A.stride(0), A.shape[1], po, out.stride(0),
+                                 out.shape[1], _stream_ptr(stream)), "mdn_stream_probe")
+    return out
 
 
 def abi_version() -> int:

@@ -1,6 +1,9 @@
 """Build libmaddness.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-    python -m paper_2106_10860_b200.build [--force] [--verbose]
+    python paper_2106_10860_b200/build.py [--force] [--verbose]
+
+Run it as a script (or via __graft_entry__.build()): `python -m` would first
+import the package, which loads -- and validates -- the current .so.
 """
 from __future__ import annotations
 

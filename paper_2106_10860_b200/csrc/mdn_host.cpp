@@ -14,6 +14,9 @@
 
 namespace mdn {
 
+cudaError_t launch_stream_probe(const float* A, int64_t N, int64_t lda, int D, float* out,
+                                int64_t ldo, int M, cudaStream_t s);
+
 uint64_t fnv1a64(const uint8_t* p, size_t n) {
   uint64_t h = 0xCBF29CE484222325ull;
   for (size_t i = 0; i < n; ++i) {
@@ -447,6 +450,15 @@ int mdn_amm_variant(const mdn_model* m, const mdn_luts* l, int64_t lda, char* bu
                                       lda, reinterpret_cast<const float*>(256), l->M);
   snprintf(buf, len, "%s", name);
   return MDN_OK;
+}
+
+int mdn_stream_probe(const float* A, int64_t N, int64_t lda, int64_t D, float* out, int64_t ldo,
+                     int64_t M, void* stream) {
+  if (N < 0 || D < 4 || D % 4 || M < 1 || lda < D || ldo < M || lda % 4) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!A || !out || (reinterpret_cast<uintptr_t>(A) & 15u)) return MDN_EINVAL;
+  return cuda_status(mdn::launch_stream_probe(A, N, lda, (int)D, out, ldo, (int)M,
+                                              (cudaStream_t)stream));
 }
 
 // ------------------------------------------------------ host executor (e2e) --

@@ -13,8 +13,8 @@ from helpers import ROOT, model_bytes
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2106_10860_b200.build import build
-    path = build()
+    import __graft_entry__
+    path = __graft_entry__._builder().build()
     return ct.CDLL(path)
 
 
@@ -114,3 +114,14 @@ def test_binding_rejects_host_tensors():
         mdn.mdn_encode(Fake(), torch.zeros(4, 32), torch.zeros(4, 2, dtype=torch.uint8))
     with pytest.raises(TypeError):
         mdn._host_ptr(np.zeros((2, 2), np.float64), "A_host")
+
+
+def test_no_unresolved_symbols(lib):
+    """Every undefined dynamic symbol of the .so is a versioned system symbol
+    (catches C/C++ linkage slips that only fail when a call is made)."""
+    import subprocess
+    from paper_2106_10860_b200 import LIB_PATH
+    out = subprocess.run(["nm", "-D", "--undefined-only", LIB_PATH], capture_output=True,
+                         text=True).stdout.split("\n")
+    bad = [l for l in out if l.strip().startswith("U ") and "@" not in l]
+    assert not bad, bad
