@@ -150,41 +150,30 @@ cudaError_t launch_amm_generic(const TreesDev& t, const LutsDev& l, const float*
 }  // namespace mdn
 
 // ---------------------------------------------------------------------------
-// Diagnostics: a plain streaming kernel with the fused path's byte mix (read
-// every element of A, write M floats per row), no table work. Its bandwidth is
-// the achievable ceiling the fused kernel is compared against.
+// Diagnostics: a plain streaming kernel with the fused path's byte mix: every
+// float of A read once (flat, fully coalesced float4 grid-stride when lda == D)
+// and N x M floats of out written once, interleaved, no table work. Its
+// bandwidth is the achievable ceiling for this read:write mix.
 namespace mdn {
 namespace {
-constexpr int PROBE_ROWS = 4;   // rows per warp iteration (loads in flight)
-
-__global__ void __launch_bounds__(256) k_stream_probe(const float* __restrict__ A, int64_t N,
-                                                      int64_t lda, int D, float* __restrict__ out,
-                                                      int64_t ldo, int M) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int D4 = D / 4;
-  for (int64_t r0 = warp * PROBE_ROWS; r0 < N; r0 += nwarps * PROBE_ROWS) {
-    float acc[PROBE_ROWS];
+__global__ void __launch_bounds__(256) k_stream_probe(const float4* __restrict__ A4, int64_t n4,
+                                                      float4* __restrict__ out4, int64_t w4) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float acc = 0.f;
+  // writes are spread evenly over the read loop: write i happens at read i * n4 / w4
+  const int64_t step = w4 > 0 ? (n4 + w4 - 1) / w4 : 0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += 4 * stride) {
+    float4 v[4];
 #pragma unroll
-    for (int k = 0; k < PROBE_ROWS; ++k) {
-      acc[k] = 0.f;
-      const int64_t r = r0 + k;
-      if (r < N) {
-        const float4* a = reinterpret_cast<const float4*>(A + r * lda);
-        for (int i = lane; i < D4; i += 32) {
-          const float4 v = __ldcs(a + i);
-          acc[k] += (v.x + v.y) + (v.z + v.w);
-        }
+    for (int u = 0; u < 4; ++u)
+      if (j + u * stride < n4) v[u] = __ldg(A4 + j + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t jj = j + u * stride;
+      if (jj < n4) {
+        acc += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+        if (step && jj % step == 0 && jj / step < w4) out4[jj / step] = make_float4(acc, acc, acc, acc);
       }
-    }
-#pragma unroll
-    for (int k = 0; k < PROBE_ROWS; ++k) {
-      float v = acc[k];
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      const int64_t r = r0 + k;
-      if (r < N)
-        for (int m = lane; m < M; m += 32) out[r * ldo + m] = v;
     }
   }
 }
@@ -194,7 +183,10 @@ cudaError_t launch_stream_probe(const float* A, int64_t N, int64_t lda, int D, f
                                 int64_t ldo, int M, cudaStream_t s) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  k_stream_probe<<<sms * 8, 256, 0, s>>>(A, N, lda, D, out, ldo, M);
+  const int64_t n4 = N * lda / 4;            // lda == D for the bench inputs
+  const int64_t w4 = N * ldo / 4;
+  k_stream_probe<<<sms * 8, 256, 0, s>>>(reinterpret_cast<const float4*>(A), n4,
+                                          reinterpret_cast<float4*>(out), w4);
   return cudaGetLastError();
 }
 }  // namespace mdn

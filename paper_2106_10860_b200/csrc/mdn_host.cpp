@@ -454,9 +454,10 @@ int mdn_amm_variant(const mdn_model* m, const mdn_luts* l, int64_t lda, char* bu
 
 int mdn_stream_probe(const float* A, int64_t N, int64_t lda, int64_t D, float* out, int64_t ldo,
                      int64_t M, void* stream) {
-  if (N < 0 || D < 4 || D % 4 || M < 1 || lda < D || ldo < M || lda % 4) return MDN_EINVAL;
+  if (N < 0 || D < 4 || D % 4 || M < 1 || lda < D || ldo < M || lda % 4 || (N * ldo) % 4) return MDN_EINVAL;
   if (N == 0) return MDN_OK;
-  if (!A || !out || (reinterpret_cast<uintptr_t>(A) & 15u)) return MDN_EINVAL;
+  if (!A || !out || (reinterpret_cast<uintptr_t>(A) & 15u) || (reinterpret_cast<uintptr_t>(out) & 15u))
+    return MDN_EINVAL;
   return cuda_status(mdn::launch_stream_probe(A, N, lda, (int)D, out, ldo, (int)M,
                                               (cudaStream_t)stream));
 }
