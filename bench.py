@@ -93,7 +93,7 @@ ORACLE_CHUNK = 16384
 def oracle_step(blk: np.ndarray, om, oluts, mode: str):
     """One oracle pass (encode + scan + dequant) over host rows."""
     import oracle as O
-    codes = O.encode(blk, om)
+    codes = O.encode_u8(blk, om) if blk.dtype == np.uint8 else O.encode(blk, om)
     S = O.scan_exact(codes, oluts.Tq) if mode == "exact" else O.scan_avg(codes, oluts.Tq, oluts.U)
     return O.dequantize(S, oluts.alpha, oluts.beta32)
 
@@ -130,7 +130,7 @@ def _bench_rows(name, rank, ws, device):
         _, n, first_chunk = shard_rows(rank, ws, spec.n_bench, CHUNK_ROWS)
         return relu_lowrank_torch(relu_W(name), n, first_chunk, device)
     import torch
-    _, A, _ = make_config_data(name, n_test=spec.n_test, n_train=0)   # 4M patches, tiled
+    _, A, _ = make_config_data(name, n_test=spec.n_test, n_train=0)   # 4M patches (f32 or u8), tiled
     reps = spec.n_bench // A.shape[0]
     return torch.from_numpy(A).to(device).repeat(reps, 1)
 
@@ -272,14 +272,18 @@ def run(args):
     codes = None
     if op != "amm":
         codes = torch.empty((n, (spec.C + 1) // 2), dtype=torch.uint8, device="cuda")
-        mdn.mdn_encode(model, A, codes)
+        (mdn.mdn_encode_u8 if A.dtype == torch.uint8 else mdn.mdn_encode)(model, A, codes)
         torch.cuda.synchronize()
+
+    u8 = A.dtype == torch.uint8
+    amm_fn = mdn.mdn_amm_u8 if u8 else mdn.mdn_amm
+    enc_fn = mdn.mdn_encode_u8 if u8 else mdn.mdn_encode
 
     def step():
         if op == "amm":
-            mdn.mdn_amm(model, luts, A, out, stream=stream)
+            amm_fn(model, luts, A, out, stream=stream)
         elif op == "encode":
-            mdn.mdn_encode(model, A, codes, stream=stream)
+            enc_fn(model, A, codes, stream=stream)
         else:
             mdn.mdn_scan(luts, codes, out=out, stream=stream)
 
@@ -306,13 +310,14 @@ def run(args):
 
     rows_total = n * ws * args.steps
     value = rows_total / (elapsed_ms / 1e3)
-    bytes_per_row = {"amm": 4 * spec.D + 4 * spec.M, "encode": 4 * spec.D + (spec.C + 1) // 2,
+    ea = A.element_size()            # 4 (fp32 A) or 1 (8-bit A)
+    bytes_per_row = {"amm": ea * spec.D + 4 * spec.M, "encode": ea * spec.D + (spec.C + 1) // 2,
                      "scan": (spec.C + 1) // 2 + 4 * spec.M}[op]
 
     # Achievable-bandwidth probe: a plain streaming kernel with the same byte
     # mix (read A, write M floats per row), timed the same way.
     probe = None
-    if op == "amm" and spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
+    if op == "amm" and not u8 and spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
         for _ in range(2):
             mdn.mdn_stream_probe(A, out, stream=stream)
         pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -340,12 +345,13 @@ def run(args):
         nmse = float(((out[:rows].double() - exact) ** 2).sum() / (exact ** 2).sum())
         torch.backends.cuda.matmul.allow_tf32 = False
         ref = torch.empty_like(out)
-        torch.matmul(A, Bd, out=ref)
+        Af = A.float() if u8 else A
+        torch.matmul(Af, Bd, out=ref)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(3):
-            torch.matmul(A, Bd, out=ref)
+            torch.matmul(Af, Bd, out=ref)
         e1.record()
         torch.cuda.synchronize()
         cublas = 3 * n / (e0.elapsed_time(e1) / 1e3)
@@ -353,7 +359,7 @@ def run(args):
 
     # --- e2e: the same metric through the public API with HOST buffers --------
     e2e = None
-    if op == "amm" and (rank == 0 or ws > 1):
+    if op == "amm" and not u8 and (rank == 0 or ws > 1):
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
                                  n_slots=3)
         n_e2e = min(n, (1 << 32) // (4 * spec.D))     # <= 4 GiB of pinned host A per rank

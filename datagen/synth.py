@@ -57,6 +57,9 @@ CONFIGS: dict[str, ConfigSpec] = {
     # configs[3]
     "image": ConfigSpec("image", "image", 32, 2, 8, 8, 0, 1_000_000, 4_000_000,
                         4_000_000 * 8, d_valid=27),
+    # the same image workload with natively 8-bit pixels
+    "image_u8": ConfigSpec("image_u8", "image_u8", 32, 2, 8, 8, 0, 1_000_000, 4_000_000,
+                           4_000_000 * 8, d_valid=27),
     # configs[4]
     "scale": ConfigSpec("scale", "relu", 256, 16, 32, 16, 32, 100_000, 1 << 24, 1 << 24),
 }
@@ -138,11 +141,30 @@ def image_patches(i: int, D: int = 32) -> np.ndarray:
     return out
 
 
-def _patch_set(first_img: int, n_rows: int, D: int) -> np.ndarray:
-    out = np.empty((n_rows, D), np.float32)
+U8_GAIN = 350.0   # blurred-noise std ~0.141 -> ~49 grey levels
+
+
+def image_patches_u8(i: int, D: int = 32) -> np.ndarray:
+    """8-bit images: pixel = clip(rint(127.5 + 350 * blurred), 0, 255); the
+    same 3x3x3 CHW windows as image_patches, zero-padded to D bytes."""
+    rng = np.random.default_rng([0, i])
+    g = _gauss_kernel()
+    chans = [np.clip(np.rint(127.5 + U8_GAIN * _blur_valid(
+        rng.standard_normal((IMG + 2 * PAD, IMG + 2 * PAD)), g)), 0, 255) for _ in range(3)]
+    n = IMG - 2
+    out = np.zeros((n * n, D), np.uint8)
+    for ch in range(3):
+        for dy in range(3):
+            for dx in range(3):
+                out[:, ch * 9 + dy * 3 + dx] = chans[ch][dy:dy + n, dx:dx + n].reshape(-1)
+    return out
+
+
+def _patch_set(first_img: int, n_rows: int, D: int, u8: bool = False) -> np.ndarray:
+    out = np.empty((n_rows, D), np.uint8 if u8 else np.float32)
     got, i = 0, first_img
     while got < n_rows:
-        p = image_patches(i, D)
+        p = image_patches_u8(i, D) if u8 else image_patches(i, D)
         take = min(n_rows - got, p.shape[0])
         out[got:got + take] = p[:take]
         got += take
@@ -181,8 +203,10 @@ def make_config_data(name: str, n_test: int | None = None, n_train: int | None =
         return A_train, A_test, B
     ntr = spec.n_train if n_train is None else n_train
     nte = spec.n_test if n_test is None else n_test
-    A_train = _patch_set(0, ntr, spec.D)
-    A_test = _patch_set(16, nte, spec.D) if nte > 0 else np.zeros((0, spec.D), np.float32)
+    u8 = spec.kind == "image_u8"
+    dt = np.uint8 if u8 else np.float32
+    A_train = _patch_set(0, ntr, spec.D, u8) if ntr > 0 else np.zeros((0, spec.D), dt)
+    A_test = _patch_set(16, nte, spec.D, u8) if nte > 0 else np.zeros((0, spec.D), dt)
     return A_train, A_test, sobel_B(spec.D)
 
 

@@ -137,6 +137,20 @@ int mdn_scan(const mdn_luts* luts, const uint8_t* codes, int64_t N, int32_t* sum
 int mdn_amm(const mdn_model* model, const mdn_luts* luts, const float* A, int64_t N,
             int64_t lda, float* out, int64_t ldo, void* stream);
 
+/* ------------------------------------------------ 8-bit input -- */
+
+/* g and the fused path for natively 8-bit A ("MADDNESS can operate on 8-bit
+ * data directly"), with App. B's 8-bit split values (L606-616):
+ * for byte inputs the x-quantiser is the identity and each threshold v becomes
+ * q = ceil(v) clamped to [0, 256], so x >= q <=> x >= v and the codes equal
+ * mdn_encode's on the same values as fp32 (reading R11).
+ *   A  device u8, N x D, row stride lda >= D (bytes). Other arguments, layouts
+ *   and errors as mdn_encode / mdn_amm. A quarter of the fp32 path's A bytes. */
+int mdn_encode_u8(const mdn_model* model, const uint8_t* A, int64_t N, int64_t lda,
+                  uint8_t* codes, void* stream);
+int mdn_amm_u8(const mdn_model* model, const mdn_luts* luts, const uint8_t* A, int64_t N,
+               int64_t lda, float* out, int64_t ldo, void* stream);
+
 /* ----------------------------------------------------- end-to-end (host) -- */
 
 /* A pipelined executor for HOST buffers: row chunks are copied host->device,

@@ -30,6 +30,7 @@ __all__ = [
     "build_G", "ridge_prototypes", "train", "build_tables", "quantize_tables",
     "beta32", "debias_constant", "mean_pair_u8", "aise_block", "scan_exact",
     "scan_avg", "dequantize", "nmse", "amm", "Luts", "make_luts", "sse_two_pass",
+    "split_values_u8", "encode_u8", "amm_u8",
 ]
 
 
@@ -139,6 +140,45 @@ def unpack_codes(packed: np.ndarray, C: int) -> np.ndarray:
     for c in range(C):
         out[:, c] = (packed[:, c // 2] >> (4 * (c % 2))) & 0xF
     return out
+
+
+# ---------------------------------------------------------------------------
+# App. B: 8-bit split values, for natively 8-bit data (L839)
+# ---------------------------------------------------------------------------
+
+def split_values_u8(model: Model) -> np.ndarray:
+    """8-bit split values for inputs that are already 8-bit integers.
+
+    App. B quantises x and v with x -> gamma_j (x - delta_j) so that line 4 of
+    Alg. 1 can compare bytes (L610-616). When the data are natively 8-bit
+    (image pixels, L839) the x-quantiser is the identity (gamma = 1,
+    delta = 0) and the threshold v must map to the integer q with
+    x >= v  <=>  x >= q for every integer x, i.e. q = ceil(v) (reading R11).
+    q is clamped to [0, 256]: v <= 0 -> 0 (every x goes right),
+    v > 255 -> 256 (every x goes left). Returns (C, 15) int64 in heap order.
+    """
+    v = np.asarray(model.thr, np.float64)
+    q = np.ceil(v)
+    return np.clip(q, 0, 256).astype(np.int64)
+
+
+def encode_u8(A_u8: np.ndarray, model: Model) -> np.ndarray:
+    """Algorithm 1 (L228-248) on uint8 rows with the 8-bit split values:
+    b <- x_{j^t} >= q^t_i, integer compare."""
+    A_u8 = np.asarray(A_u8)
+    assert A_u8.dtype == np.uint8
+    q = split_values_u8(model)
+    N = A_u8.shape[0]
+    codes = np.empty((N, model.C), np.uint8)
+    for c in range(model.C):
+        levels = [q[c, (1 << t) - 1:(1 << (t + 1)) - 1] for t in range(LEVELS)]
+        i = np.ones(N, np.int64)                                         # L233
+        for t in range(1, LEVELS + 1):                                   # L235
+            qq = levels[t - 1][i - 1]                                    # L239
+            b = (A_u8[:, model.dims[c, t - 1]].astype(np.int64) >= qq).astype(np.int64)  # L240
+            i = 2 * i - 1 + b                                            # L242
+        codes[:, c] = (i - 1).astype(np.uint8)
+    return codes
 
 
 # ---------------------------------------------------------------------------
@@ -495,6 +535,16 @@ def dequantize(S: np.ndarray, alpha: np.float32, beta: np.float32) -> np.ndarray
 def amm(A: np.ndarray, model: Model, luts: Luts):
     """Full inference: codes, integer sums, fp32 output."""
     codes = encode(A, model)
+    if luts.mode == "exact":
+        S = scan_exact(codes, luts.Tq)
+    else:
+        S = scan_avg(codes, luts.Tq, luts.U)
+    return codes, S, dequantize(S, luts.alpha, luts.beta32)
+
+
+def amm_u8(A_u8: np.ndarray, model: Model, luts: Luts):
+    """Full inference on 8-bit rows: encode_u8, then the same f and dequant."""
+    codes = encode_u8(A_u8, model)
     if luts.mode == "exact":
         S = scan_exact(codes, luts.Tq)
     else:

@@ -53,6 +53,8 @@ _SIGS = {
     "mdn_abi_version": (_i32, []),
     "mdn_amm_variant": (_i32, [_vp, _vp, _i64, ct.c_char_p, _sz]),
     "mdn_stream_probe": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
+    "mdn_encode_u8": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
+    "mdn_amm_u8": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -217,6 +219,28 @@ def mdn_amm(model: Model, luts: Luts, A, out, stream=None):
         raise ValueError("out must be N x M")
     _check(_lib.mdn_amm(model._h, luts._h, pa, A.shape[0], A.stride(0), po, out.stride(0),
                         _stream_ptr(stream)), "mdn_amm")
+    return out
+
+
+def mdn_encode_u8(model: Model, A, codes, stream=None):
+    """g for natively 8-bit A (App. B 8-bit split values)."""
+    pa = _dev_ptr(A, "uint8", "A")
+    pc = _dev_ptr(codes, "uint8", "codes")
+    if codes.shape != (A.shape[0], (model.C + 1) // 2) or not codes.is_contiguous():
+        raise ValueError("codes must be contiguous N x ceil(C/2)")
+    _check(_lib.mdn_encode_u8(model._h, pa, A.shape[0], A.stride(0), pc, _stream_ptr(stream)),
+           "mdn_encode_u8")
+    return codes
+
+
+def mdn_amm_u8(model: Model, luts: Luts, A, out, stream=None):
+    """Fused g + f + dequant for natively 8-bit A."""
+    pa = _dev_ptr(A, "uint8", "A")
+    po = _dev_ptr(out, "float32", "out")
+    if out.shape != (A.shape[0], luts.M):
+        raise ValueError("out must be N x M")
+    _check(_lib.mdn_amm_u8(model._h, luts._h, pa, A.shape[0], A.stride(0), po, out.stride(0),
+                           _stream_ptr(stream)), "mdn_amm_u8")
     return out
 
 

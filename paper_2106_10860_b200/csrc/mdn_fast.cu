@@ -60,7 +60,8 @@ struct Params {
   int64_t n_tiles;
   int64_t ldo;
   int D, SW, nslab, R, NS;
-  int slab_words;                 // shared-memory words per slab (128-B aligned)
+  int slab_e;                     // shared-memory elements (of the input type) per slab, 128-B aligned
+  int pad_e;                      // row pitch = SW + pad_e elements (16 bytes of padding)
   int M;
   int l2_hint;                    // 0 none (default), 1 evict_first, 2 evict_last, 3 evict_normal
   float alpha_eff, beta32;
@@ -68,6 +69,7 @@ struct Params {
   const uint16_t* dims;           // global [C][4]
   const uint16_t* sub;            // global [C] subspace begin
   const float* thr;               // global [C][16]
+  const uint16_t* q;              // global [C][16] 8-bit split values ceil(v) (uint8 input)
   float* out;
   uint8_t* codes;                 // encode-only output
 };
@@ -237,20 +239,65 @@ __device__ __forceinline__ float pick4(const float4& v, int s) {
   return (s & 2) ? b : a;
 }
 
-// SUBF = 0: the 4 split-dim values are read one by one (s_off: word offsets).
-// SUBF = 1 / 2: the codebook's whole subspace (<= 4 / <= 8 columns, 16-B
-// aligned) is read with 1 / 2 conflict-free LDS.128 (row pitch == 4 mod 32
-// words) and the split dims picked with warp-uniform selects (s_off: column
-// within the subspace, s_base: subspace word offset) -- 4x / 2x fewer shared
-// wavefronts than four 4-way-conflicted LDS.32.
-template <int C, int SUBF>
-__device__ __forceinline__ uint32_t encode_group(const float* __restrict__ rowp,
+// fp32 input (TIn = float):
+//   SUBF = 0: the 4 split-dim values are read one by one (s_off: offsets).
+//   SUBF = 1 / 2: the codebook's whole subspace (<= 4 / <= 8 columns, 16-B
+//   aligned) is read with 1 / 2 conflict-free LDS.128 (row pitch == 4 mod 32
+//   words) and the split dims picked with warp-uniform selects (s_off: column
+//   within the subspace, s_base: subspace offset) -- 4x / 2x fewer shared
+//   wavefronts than four 4-way-conflicted LDS.32.
+// 8-bit input (TIn = uint8_t): thresholds are the
+// integer split values q = ceil(v) (App. B, reading R11) and x >= q is an
+//   integer compare. SUBF = 1 / 2: every subspace is exactly 4 / 8 bytes, so
+//   the unit's G codebooks occupy 4G / 8G contiguous bytes, fetched with
+//   LDS.128 and split into bytes with PRMT.
+__device__ __forceinline__ uint32_t byte_of(uint32_t lo, uint32_t hi, int sel) {
+  return __byte_perm(lo, hi, (uint32_t)sel) & 0xFFu;     // byte sel (0..7) of {hi:lo}
+}
+
+template <class TIn, int C, int SUBF>
+__device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
                                                  const int* __restrict__ s_off,
                                                  const int* __restrict__ s_base,
                                                  const float* __restrict__ s_thr, int c0) {
+  constexpr int G = C >= 8 ? 8 : C;
   uint32_t word = 0;
+  if constexpr (sizeof(TIn) == 1) {
+    const int* s_q = reinterpret_cast<const int*>(s_thr);
+    uint32_t wv[SUBF == 0 ? 1 : G * SUBF];
+    if constexpr (SUBF > 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(rowp + s_base[c0]);
 #pragma unroll
-  for (int i = 0; i < (C >= 8 ? 8 : C); ++i) {
+      for (int k = 0; k < G * SUBF / 4; ++k) {
+        const uint4 v = src[k];
+        wv[4 * k] = v.x, wv[4 * k + 1] = v.y, wv[4 * k + 2] = v.z, wv[4 * k + 3] = v.w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int c = c0 + i;
+      const int4 o = *reinterpret_cast<const int4*>(s_off + 4 * c);
+      int x0, x1, x2, x3;
+      if constexpr (SUBF == 0) {
+        x0 = rowp[o.x], x1 = rowp[o.y], x2 = rowp[o.z], x3 = rowp[o.w];
+      } else if constexpr (SUBF == 1) {
+        x0 = byte_of(wv[i], 0u, o.x), x1 = byte_of(wv[i], 0u, o.y);
+        x2 = byte_of(wv[i], 0u, o.z), x3 = byte_of(wv[i], 0u, o.w);
+      } else {
+        x0 = byte_of(wv[2 * i], wv[2 * i + 1], o.x), x1 = byte_of(wv[2 * i], wv[2 * i + 1], o.y);
+        x2 = byte_of(wv[2 * i], wv[2 * i + 1], o.z), x3 = byte_of(wv[2 * i], wv[2 * i + 1], o.w);
+      }
+      const int* th = s_q + 16 * c;
+      uint32_t p = x0 >= th[0] ? 1u : 0u;
+      p = 2u * p + (x1 >= th[1 + p] ? 1u : 0u);
+      p = 2u * p + (x2 >= th[3 + p] ? 1u : 0u);
+      p = 2u * p + (x3 >= th[7 + p] ? 1u : 0u);
+      word |= p << (4 * i);
+    }
+    return word;
+  } else {
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
     const int c = c0 + i;
     const int4 o = *reinterpret_cast<const int4*>(s_off + 4 * c);
     float x0, x1, x2, x3;
@@ -278,9 +325,10 @@ __device__ __forceinline__ uint32_t encode_group(const float* __restrict__ rowp,
     word |= p << (4 * i);
   }
   return word;
+  }
 }
 
-template <int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF>
+template <class TIn, int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF>
 __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
     k_amm_ws(const __grid_constant__ CUtensorMap tmap, const Params p) {
   constexpr int G = C >= 8 ? 8 : C;      // codebooks per encoder unit (one code word)
@@ -307,20 +355,25 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
   int* s_base = reinterpret_cast<int*>(smem + OFF_BASE);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
   uint32_t* s_codes = reinterpret_cast<uint32_t*>(smem + OFF_CODES);
-  float* s_stage = reinterpret_cast<float*>(smem + OFF_STAGE);
+  TIn* s_stage = reinterpret_cast<TIn*>(smem + OFF_STAGE);
   const int tid = threadIdx.x;
-  const int pitch = p.SW + 4;
-  const int stage_words = p.nslab * p.slab_words;
+  const int pitch = p.SW + p.pad_e;                 // elements of TIn per shared row
+  const int stage_e = p.nslab * p.slab_e;
 
   // ---- setup: trees, split-dim offsets, tables, barriers ----
-  for (int i = tid; i < 16 * C; i += blockDim.x) s_thr[i] = p.thr[i];
+  for (int i = tid; i < 16 * C; i += blockDim.x) {
+    if constexpr (sizeof(TIn) == 1)
+      reinterpret_cast<int*>(s_thr)[i] = p.q[i];   // integer split values (App. B, R11)
+    else
+      s_thr[i] = p.thr[i];
+  }
   for (int i = tid; i < 4 * C; i += blockDim.x) {
     const int d = p.dims[i];
-    s_off[i] = SUBF ? d - p.sub[i / 4] : (d / p.SW) * p.slab_words + (d % p.SW);
+    s_off[i] = SUBF ? d - p.sub[i / 4] : (d / p.SW) * p.slab_e + (d % p.SW);
   }
   for (int c = tid; c < C; c += blockDim.x) {
     const int b = p.sub[c];
-    s_base[c] = (b / p.SW) * p.slab_words + (b % p.SW);
+    s_base[c] = (b / p.SW) * p.slab_e + (b % p.SW);
   }
   if constexpr (!ENC_ONLY) {
     const uint4* src = reinterpret_cast<const uint4*>(p.lut);
@@ -346,7 +399,7 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(p.nslab * p.R * pitch * 4);
+      const uint32_t bytes = (uint32_t)(p.nslab * p.R * pitch * sizeof(TIn));
       const uint64_t pol = l2_policy(p.l2_hint);
       uint32_t q = 0;
       for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
@@ -359,9 +412,9 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
             continue;
           }
           mbar_arrive_tx(&full[s], bytes);
-          float* dst = s_stage + (size_t)s * stage_words;
+          TIn* dst = s_stage + (size_t)s * stage_e;
           for (int k = 0; k < p.nslab; ++k)
-            tma_load_2d(dst + k * p.slab_words, &tmap, k * p.SW, (int)y, &full[s], p.l2_hint, pol);
+            tma_load_2d(dst + k * p.slab_e, &tmap, k * p.SW, (int)y, &full[s], p.l2_hint, pol);
         }
       }
     }
@@ -375,10 +428,10 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
       for (int st = 0; st < stages_per_tile; ++st, ++q) {
         const int s = q % p.NS;
         mbar_wait(&full[s], (q / p.NS) & 1u);
-        const float* stg = s_stage + (size_t)s * stage_words;
+        const TIn* stg = s_stage + (size_t)s * stage_e;
         for (int u = etid; u < p.R * NG; u += EW * 32) {
           const int r = u % p.R, g = u / p.R;
-          const uint32_t word = encode_group<C, SUBF>(stg + r * pitch, s_off, s_base, s_thr, g * G);
+          const uint32_t word = encode_group<TIn, C, SUBF>(stg + r * pitch, s_off, s_base, s_thr, g * G);
           const int row_local = st * p.R + r;
           if constexpr (ENC_ONLY) {
             const int64_t row = tile * BR + row_local;
@@ -495,40 +548,44 @@ DevInfo dev_info() {
 
 struct Geometry {
   bool ok = false;
-  int SW, nslab, R, NS, slab_words;
+  int SW, nslab, R, NS, slab_e, pad_e;
   size_t smem;
 };
 
-// Slab width SW (<= 252 so that a box of SW + 4 columns fits the 256-element
-// TMA box limit) dividing D, then the largest rows-per-stage R (dividing the
-// 256-row tile) that leaves room for >= 4 stages (>= 2 at worst).
-Geometry plan(int C, int W, int D, bool enc_only) {
+// Slab width SW dividing D such that a box of SW + pad_e elements (pad_e =
+// 16 bytes of padding) fits the 256-element TMA box limit and is a multiple of
+// 16 bytes; then the largest rows-per-stage R (dividing the 256-row tile) that
+// leaves room for >= 4 stages (>= 2 at worst). es = input element size.
+Geometry plan(int C, int W, int D, bool enc_only, int es) {
   Geometry g;
-  if (D % 4 != 0) return g;
+  const int pad_e = 16 / es;
+  if (D % pad_e != 0) return g;
   int nslab = 0;
   for (int n = 1; n <= 64; ++n)
-    if (D % n == 0 && (D / n) % 4 == 0 && D / n <= 252) {
+    if (D % n == 0 && (D / n) % pad_e == 0 && D / n + pad_e <= 256) {
       nslab = n;
       break;
     }
   if (!nslab) return g;
   g.nslab = nslab;
   g.SW = D / nslab;
+  g.pad_e = pad_e;
   const int CBW = C >= 8 ? C / 8 : 1;
   size_t fixed = BAR_BYTES + 16 * C * 4 + 4 * C * 4 + C * 4 + 16;
   if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4;
   fixed = (fixed + 127) & ~size_t(127);
   const size_t budget = (size_t)dev_info().smem_optin;
+  const int align_e = 128 / es;
   for (int min_ns : {4, 2}) {
     for (int R : {256, 128, 64, 32, 16, 8}) {
-      int slab_words = ((R * (g.SW + 4)) + 31) & ~31;
-      size_t stage = (size_t)nslab * slab_words * 4;
+      int slab_e = ((R * (g.SW + pad_e)) + align_e - 1) / align_e * align_e;
+      size_t stage = (size_t)nslab * slab_e * es;
       if (fixed + stage * min_ns > budget) continue;
       int NS = (int)((budget - fixed) / stage);
       if (NS > NS_MAX) NS = NS_MAX;
       g.R = R;
       g.NS = NS;
-      g.slab_words = slab_words;
+      g.slab_e = slab_e;
       g.smem = fixed + stage * NS;
       g.ok = true;
       return g;
@@ -552,7 +609,8 @@ int knob_hint() {
   return v;
 }
 
-bool make_tmap(CUtensorMap* m, const float* A, int64_t N, int64_t lda, int D, int SW, int R) {
+bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int SW, int R,
+               int es) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   const int pr = knob_promo();
@@ -562,17 +620,18 @@ bool make_tmap(CUtensorMap* m, const float* A, int64_t N, int64_t lda, int D, in
                          : pr == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                      : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)N};
-  cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
-  cuuint32_t box[2] = {(cuuint32_t)(SW + 4), (cuuint32_t)R};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * es};
+  cuuint32_t box[2] = {(cuuint32_t)(SW + 16 / es), (cuuint32_t)R};
   cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
+  return fn(m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+            const_cast<void*>(A), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int C, int W, int U, bool VEC, bool ENC, int SUBF>
+template <class TIn, int C, int W, int U, bool VEC, bool ENC, int SUBF>
 cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
-  auto k = k_amm_ws<C, W, U, VEC, ENC, SUBF>;
+  auto k = k_amm_ws<TIn, C, W, U, VEC, ENC, SUBF>;
   // Per launch: the attribute is per device context and costs ~1 us.
   cudaError_t attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr_err != cudaSuccess) return attr_err;
@@ -582,14 +641,14 @@ cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cu
 }
 
 // Subspace-vector encoders are compiled for the small-D tables (C <= 8).
-template <int C, int W, int U, bool VEC, bool ENC>
+template <class TIn, int C, int W, int U, bool VEC, bool ENC>
 cudaError_t launch_ws_t(const CUtensorMap& tm, const Params& p, int subf, size_t smem,
                         cudaStream_t s) {
   if constexpr (C <= 8) {
-    if (subf == 1) return launch_ws_sf<C, W, U, VEC, ENC, 1>(tm, p, smem, s);
-    if (subf == 2) return launch_ws_sf<C, W, U, VEC, ENC, 2>(tm, p, smem, s);
+    if (subf == 1) return launch_ws_sf<TIn, C, W, U, VEC, ENC, 1>(tm, p, smem, s);
+    if (subf == 2) return launch_ws_sf<TIn, C, W, U, VEC, ENC, 2>(tm, p, smem, s);
   }
-  return launch_ws_sf<C, W, U, VEC, ENC, 0>(tm, p, smem, s);
+  return launch_ws_sf<TIn, C, W, U, VEC, ENC, 0>(tm, p, smem, s);
 }
 
 template <int C, int W, int U, bool VEC>
@@ -631,31 +690,36 @@ using namespace fast;
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-static bool amm_fast_ok(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
+// es = input element size (4: fp32 A, 1: uint8 A).
+static int subf_for(const TreesDev& t, const Geometry& g, int es) {
+  if (g.nslab != 1) return 0;                 // subspace loads stay inside one slab
+  return es == 4 ? t.subf : t.subf_u8;
+}
+
+static bool amm_fast_ok(const TreesDev& t, const LutsDev& l, const void* A, int64_t lda, int es,
                         Geometry* geo) {
   if (!has_combo(t.C, l.W, l.U)) return false;
-  if (!aligned16(A) || lda % 4 != 0) return false;
+  if (!aligned16(A) || (lda * es) % 16 != 0) return false;
   if (!encode_fn()) return false;
-  *geo = plan(t.C, l.W, t.D, false);
+  *geo = plan(t.C, l.W, t.D, false, es);
   return geo->ok;
 }
 
 const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
                              const float* out, int64_t ldo) {
   Geometry g;
-  if (!amm_fast_ok(t, l, A, lda, &g)) return "generic";
+  if (!amm_fast_ok(t, l, A, lda, 4, &g)) return "generic";
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
-  const int sf = g.nslab == 1 ? t.subf : 0;
   static const char* names[2][3] = {{"ws_tma", "ws_tma_sub4", "ws_tma_sub8"},
                                     {"ws_tma_vec", "ws_tma_vec_sub4", "ws_tma_vec_sub8"}};
-  return names[vec][sf];
+  return names[vec][subf_for(t, g, 4)];
 }
 
-cudaError_t launch_encode_generic(const TreesDev&, const float*, int64_t, int64_t, uint8_t*,
+cudaError_t launch_encode_generic(const TreesDev&, const void*, int, int64_t, int64_t, uint8_t*,
                                   cudaStream_t);
 cudaError_t launch_scan_generic(const LutsDev&, const uint8_t*, int64_t, int32_t*, float*, int64_t,
                                 cudaStream_t);
-cudaError_t launch_amm_generic(const TreesDev&, const LutsDev&, const float*, int64_t, int64_t,
+cudaError_t launch_amm_generic(const TreesDev&, const LutsDev&, const void*, int, int64_t, int64_t,
                                float*, int64_t, cudaStream_t);
 
 static Params base_params(const TreesDev& t, const Geometry& g, int64_t N) {
@@ -667,23 +731,27 @@ static Params base_params(const TreesDev& t, const Geometry& g, int64_t N) {
   p.nslab = g.nslab;
   p.R = g.R;
   p.NS = g.NS;
-  p.slab_words = g.slab_words;
+  p.slab_e = g.slab_e;
+  p.pad_e = g.pad_e;
   p.dims = t.dims;
   p.sub = t.sub;
   p.l2_hint = knob_hint();
   p.thr = t.thr;
+  p.q = t.q;
   return p;
 }
 
-cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int64_t N, int64_t lda,
-                       float* out, int64_t ldo, cudaStream_t s) {
+template <class TIn>
+static cudaError_t amm_fast(const TreesDev& t, const LutsDev& l, const TIn* A, int64_t N,
+                            int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done) {
+  constexpr int es = sizeof(TIn);
+  *done = false;
   Geometry g;
-  if (N > (int64_t)0x7FFFFF00 || !amm_fast_ok(t, l, A, lda, &g))
-    return launch_amm_generic(t, l, A, N, lda, out, ldo, s);
+  if (N > (int64_t)0x7FFFFF00 || !amm_fast_ok(t, l, A, lda, es, &g)) return cudaSuccess;
   CUtensorMap tm;
-  if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R)) return launch_amm_generic(t, l, A, N, lda, out, ldo, s);
+  if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R, es)) return cudaSuccess;
   Params p = base_params(t, g, N);
-  const int sf = g.nslab == 1 ? t.subf : 0;   // subspace loads stay inside one slab
+  const int sf = subf_for(t, g, es);
   p.ldo = ldo;
   p.M = l.M;
   p.alpha_eff = l.alpha_eff;
@@ -691,36 +759,72 @@ cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int6
   p.lut = l.words;
   p.out = out;
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
-#define X(c, w, u)                                                             \
-  if (t.C == c && l.W == w && l.U == u)                                        \
-    return vec ? launch_ws_t<c, w, u, true, false>(tm, p, sf, g.smem, s)       \
-               : launch_ws_t<c, w, u, false, false>(tm, p, sf, g.smem, s);
+  *done = true;
+#define X(c, w, u)                                                                  \
+  if (t.C == c && l.W == w && l.U == u)                                             \
+    return vec ? launch_ws_t<TIn, c, w, u, true, false>(tm, p, sf, g.smem, s)       \
+               : launch_ws_t<TIn, c, w, u, false, false>(tm, p, sf, g.smem, s);
   MDN_FAST_COMBOS(X)
 #undef X
-  return launch_amm_generic(t, l, A, N, lda, out, ldo, s);
+  *done = false;
+  return cudaSuccess;
+}
+
+template <class TIn>
+static cudaError_t encode_fast(const TreesDev& t, const TIn* A, int64_t N, int64_t lda,
+                               uint8_t* codes, cudaStream_t s, bool* done) {
+  constexpr int es = sizeof(TIn);
+  *done = false;
+  if (N > (int64_t)0x7FFFFF00 || !has_encoder(t.C) || !aligned16(A) || (lda * es) % 16 != 0 ||
+      !encode_fn())
+    return cudaSuccess;
+  if (t.C >= 8 && (reinterpret_cast<uintptr_t>(codes) & 3u)) return cudaSuccess;
+  if (t.C == 4 && (reinterpret_cast<uintptr_t>(codes) & 1u)) return cudaSuccess;
+  Geometry g = plan(t.C, 1, t.D, true, es);
+  if (!g.ok) return cudaSuccess;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R, es)) return cudaSuccess;
+  Params p = base_params(t, g, N);
+  const int sf = subf_for(t, g, es);
+  p.codes = codes;
+  *done = true;
+  switch (t.C) {
+    case 4: return launch_ws_t<TIn, 4, 1, 0, false, true>(tm, p, sf, g.smem, s);
+    case 8: return launch_ws_t<TIn, 8, 1, 0, false, true>(tm, p, sf, g.smem, s);
+    case 16: return launch_ws_t<TIn, 16, 1, 0, false, true>(tm, p, sf, g.smem, s);
+    case 32: return launch_ws_t<TIn, 32, 1, 0, false, true>(tm, p, sf, g.smem, s);
+    case 64: return launch_ws_t<TIn, 64, 1, 0, false, true>(tm, p, sf, g.smem, s);
+  }
+  *done = false;
+  return cudaSuccess;
+}
+
+cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int64_t N, int64_t lda,
+                       float* out, int64_t ldo, cudaStream_t s) {
+  bool done;
+  cudaError_t e = amm_fast<float>(t, l, A, N, lda, out, ldo, s, &done);
+  return done ? e : launch_amm_generic(t, l, A, 4, N, lda, out, ldo, s);
+}
+
+cudaError_t launch_amm_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
+                          int64_t lda, float* out, int64_t ldo, cudaStream_t s) {
+  bool done;
+  cudaError_t e = amm_fast<uint8_t>(t, l, A, N, lda, out, ldo, s, &done);
+  return done ? e : launch_amm_generic(t, l, A, 1, N, lda, out, ldo, s);
 }
 
 cudaError_t launch_encode(const TreesDev& t, const float* A, int64_t N, int64_t lda, uint8_t* codes,
                           cudaStream_t s) {
-  if (N > (int64_t)0x7FFFFF00 || !has_encoder(t.C) || !aligned16(A) || lda % 4 != 0 || !encode_fn())
-    return launch_encode_generic(t, A, N, lda, codes, s);
-  if (t.C >= 8 && (reinterpret_cast<uintptr_t>(codes) & 3u)) return launch_encode_generic(t, A, N, lda, codes, s);
-  if (t.C == 4 && (reinterpret_cast<uintptr_t>(codes) & 1u)) return launch_encode_generic(t, A, N, lda, codes, s);
-  Geometry g = plan(t.C, 1, t.D, true);
-  if (!g.ok) return launch_encode_generic(t, A, N, lda, codes, s);
-  CUtensorMap tm;
-  if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R)) return launch_encode_generic(t, A, N, lda, codes, s);
-  Params p = base_params(t, g, N);
-  const int sf = g.nslab == 1 ? t.subf : 0;
-  p.codes = codes;
-  switch (t.C) {
-    case 4: return launch_ws_t<4, 1, 0, false, true>(tm, p, sf, g.smem, s);
-    case 8: return launch_ws_t<8, 1, 0, false, true>(tm, p, sf, g.smem, s);
-    case 16: return launch_ws_t<16, 1, 0, false, true>(tm, p, sf, g.smem, s);
-    case 32: return launch_ws_t<32, 1, 0, false, true>(tm, p, sf, g.smem, s);
-    case 64: return launch_ws_t<64, 1, 0, false, true>(tm, p, sf, g.smem, s);
-  }
-  return launch_encode_generic(t, A, N, lda, codes, s);
+  bool done;
+  cudaError_t e = encode_fast<float>(t, A, N, lda, codes, s, &done);
+  return done ? e : launch_encode_generic(t, A, 4, N, lda, codes, s);
+}
+
+cudaError_t launch_encode_u8(const TreesDev& t, const uint8_t* A, int64_t N, int64_t lda,
+                             uint8_t* codes, cudaStream_t s) {
+  bool done;
+  cudaError_t e = encode_fast<uint8_t>(t, A, N, lda, codes, s, &done);
+  return done ? e : launch_encode_generic(t, A, 1, N, lda, codes, s);
 }
 
 cudaError_t launch_scan(const LutsDev& l, const uint8_t* codes, int64_t N, int32_t* sums,

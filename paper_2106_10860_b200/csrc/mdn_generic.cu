@@ -13,6 +13,8 @@ constexpr int GEN_THREADS = 256;
 
 // Algorithm 1 for one codebook of one row:
 // p <- 2p + [x_{j^t} >= v^t_p], t = 1..4 (0-based heap node 2^t - 1 + p).
+// fp32 A: x >= v in fp32. uint8 A: x >= q with the integer split
+// values q = ceil(v) (App. B, reading R11), stored in s_thr as ints.
 __device__ __forceinline__ int hash_row(const float* __restrict__ a, const int* s_dims,
                                         const float* s_thr, int c) {
   int p = 0;
@@ -25,22 +27,42 @@ __device__ __forceinline__ int hash_row(const float* __restrict__ a, const int* 
   return p;
 }
 
-__device__ __forceinline__ void load_trees(const TreesDev& t, int* s_dims, float* s_thr) {
-  for (int i = threadIdx.x; i < t.C * 4; i += blockDim.x) s_dims[i] = t.dims[i];
-  for (int i = threadIdx.x; i < t.C * THR_STRIDE; i += blockDim.x) s_thr[i] = t.thr[i];
+__device__ __forceinline__ int hash_row(const uint8_t* __restrict__ a, const int* s_dims,
+                                        const float* s_thr, int c) {
+  const int* s_q = reinterpret_cast<const int*>(s_thr);
+  int p = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    int x = __ldg(a + s_dims[c * 4 + t]);
+    int q = s_q[c * THR_STRIDE + (1 << t) - 1 + p];
+    p = 2 * p + (x >= q ? 1 : 0);
+  }
+  return p;
 }
 
-__global__ void k_encode_generic(TreesDev t, const float* __restrict__ A, int64_t N, int64_t lda,
+template <class TIn>
+__device__ __forceinline__ void load_trees(const TreesDev& t, int* s_dims, float* s_thr) {
+  for (int i = threadIdx.x; i < t.C * 4; i += blockDim.x) s_dims[i] = t.dims[i];
+  for (int i = threadIdx.x; i < t.C * THR_STRIDE; i += blockDim.x) {
+    if constexpr (sizeof(TIn) == 1)
+      reinterpret_cast<int*>(s_thr)[i] = t.q[i];
+    else
+      s_thr[i] = t.thr[i];
+  }
+}
+
+template <class TIn>
+__global__ void k_encode_generic(TreesDev t, const TIn* __restrict__ A, int64_t N, int64_t lda,
                                  uint8_t* __restrict__ codes) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_thr = reinterpret_cast<float*>(smem);
   int* s_dims = reinterpret_cast<int*>(s_thr + t.C * THR_STRIDE);
-  load_trees(t, s_dims, s_thr);
+  load_trees<TIn>(t, s_dims, s_thr);
   __syncthreads();
   const int nb = (t.C + 1) / 2;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < N;
        row += (int64_t)gridDim.x * blockDim.x) {
-    const float* a = A + row * lda;
+    const TIn* a = A + row * lda;
     uint8_t* out = codes + row * nb;
     for (int c = 0; c < t.C; c += 2) {
       int lo = hash_row(a, s_dims, s_thr, c);
@@ -96,17 +118,18 @@ __global__ void k_scan_generic(LutsDev l, const uint8_t* __restrict__ codes, int
   }
 }
 
-__global__ void k_amm_generic(TreesDev t, LutsDev l, const float* __restrict__ A, int64_t N,
+template <class TIn>
+__global__ void k_amm_generic(TreesDev t, LutsDev l, const TIn* __restrict__ A, int64_t N,
                               int64_t lda, float* __restrict__ out, int64_t ldo) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_thr = reinterpret_cast<float*>(smem);
   int* s_dims = reinterpret_cast<int*>(s_thr + t.C * THR_STRIDE);
-  load_trees(t, s_dims, s_thr);
+  load_trees<TIn>(t, s_dims, s_thr);
   __syncthreads();
   uint8_t code_row[MAX_C / 2];
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < N;
        row += (int64_t)gridDim.x * blockDim.x) {
-    const float* a = A + row * lda;
+    const TIn* a = A + row * lda;
     for (int c = 0; c < t.C; c += 2) {
       int lo = hash_row(a, s_dims, s_thr, c);
       int hi = c + 1 < t.C ? hash_row(a, s_dims, s_thr, c + 1) : 0;
@@ -127,10 +150,15 @@ unsigned grid_for(int64_t N) {
 
 }  // namespace
 
-cudaError_t launch_encode_generic(const TreesDev& t, const float* A, int64_t N, int64_t lda,
+cudaError_t launch_encode_generic(const TreesDev& t, const void* A, int es, int64_t N, int64_t lda,
                                   uint8_t* codes, cudaStream_t s) {
   size_t sm = (size_t)t.C * (THR_STRIDE * 4 + 16);
-  k_encode_generic<<<grid_for(N), GEN_THREADS, sm, s>>>(t, A, N, lda, codes);
+  if (es == 1)
+    k_encode_generic<uint8_t><<<grid_for(N), GEN_THREADS, sm, s>>>(
+        t, static_cast<const uint8_t*>(A), N, lda, codes);
+  else
+    k_encode_generic<float><<<grid_for(N), GEN_THREADS, sm, s>>>(
+        t, static_cast<const float*>(A), N, lda, codes);
   return cudaGetLastError();
 }
 
@@ -140,10 +168,15 @@ cudaError_t launch_scan_generic(const LutsDev& l, const uint8_t* codes, int64_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_amm_generic(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
-                               int64_t lda, float* out, int64_t ldo, cudaStream_t s) {
+cudaError_t launch_amm_generic(const TreesDev& t, const LutsDev& l, const void* A, int es,
+                               int64_t N, int64_t lda, float* out, int64_t ldo, cudaStream_t s) {
   size_t sm = (size_t)t.C * (THR_STRIDE * 4 + 16);
-  k_amm_generic<<<grid_for(N), GEN_THREADS, sm, s>>>(t, l, A, N, lda, out, ldo);
+  if (es == 1)
+    k_amm_generic<uint8_t><<<grid_for(N), GEN_THREADS, sm, s>>>(
+        t, l, static_cast<const uint8_t*>(A), N, lda, out, ldo);
+  else
+    k_amm_generic<float><<<grid_for(N), GEN_THREADS, sm, s>>>(
+        t, l, static_cast<const float*>(A), N, lda, out, ldo);
   return cudaGetLastError();
 }
 

@@ -129,6 +129,7 @@ void mdn_model_free(mdn_model* m) {
     cudaFree(m->d_thr);
     cudaFree(m->d_P);
     cudaFree(m->d_sub);
+    cudaFree(m->d_q);
   }
   delete m;
 }
@@ -177,6 +178,20 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
     }
   }
   m->subf = aligned && max_w <= 4 ? 1 : (aligned && max_w <= 8 ? 2 : 0);
+  // uint8 input: every subspace exactly 4 (or 8) bytes, back to back
+  m->subf_u8 = 0;
+  for (int w : {4, 8}) {
+    bool ok = (int)D == w * (int)C;
+    for (uint32_t c = 0; c < C && ok; ++c) ok = m->h_sub[c] == w * c;
+    if (ok) m->subf_u8 = w / 4;
+  }
+  // App. B 8-bit split values for natively 8-bit x (reading R11): q = ceil(v),
+  // clamped to [0, 256] so that x >= q <=> x >= v for every byte x.
+  m->h_q.assign((size_t)C * THR_STRIDE, 0);
+  for (size_t i = 0; i < m->h_q.size(); ++i) {
+    double q = std::ceil((double)m->h_thr[i]);
+    m->h_q[i] = (uint16_t)(q < 0 ? 0 : (q > 256 ? 256 : q));
+  }
   size_t p_bytes = (size_t)K * C * D * sizeof(float);
   if (!r.need(p_bytes + 8)) return set_err(err_off, r.fail_off, MDN_EFORMAT);
   const uint8_t* P = r.p + r.off;
@@ -195,7 +210,8 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
     return st;
   }
   if ((st = dalloc(&m->d_P, (size_t)K * C * D)) != MDN_OK ||
-      (st = dalloc(&m->d_sub, (size_t)C)) != MDN_OK) {
+      (st = dalloc(&m->d_sub, (size_t)C)) != MDN_OK ||
+      (st = dalloc(&m->d_q, m->h_q.size())) != MDN_OK) {
     mdn_model_free(m.release());
     return st;
   }
@@ -203,7 +219,9 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   cudaError_t e2 = cudaMemcpy(m->d_thr, m->h_thr.data(), m->h_thr.size() * 4, cudaMemcpyHostToDevice);
   cudaError_t e3 = cudaMemcpy(m->d_P, P, p_bytes, cudaMemcpyHostToDevice);
   cudaError_t e4 = cudaMemcpy(m->d_sub, m->h_sub.data(), C * 2, cudaMemcpyHostToDevice);
-  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
+  cudaError_t e5 = cudaMemcpy(m->d_q, m->h_q.data(), m->h_q.size() * 2, cudaMemcpyHostToDevice);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess ||
+      e5 != cudaSuccess) {
     mdn_model_free(m.release());
     return MDN_ECUDA;
   }
@@ -441,6 +459,30 @@ int mdn_amm(const mdn_model* m, const mdn_luts* l, const float* A, int64_t N, in
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
   return cuda_status(launch_amm(m->trees(), l->dev(), A, N, lda, out, ldo, (cudaStream_t)stream));
+}
+
+int mdn_encode_u8(const mdn_model* m, const uint8_t* A, int64_t N, int64_t lda, uint8_t* codes,
+                  void* stream) {
+  if (!m || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!A || !codes || lda < m->D) return MDN_EINVAL;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  return cuda_status(launch_encode_u8(m->trees(), A, N, lda, codes, (cudaStream_t)stream));
+}
+
+int mdn_amm_u8(const mdn_model* m, const mdn_luts* l, const uint8_t* A, int64_t N, int64_t lda,
+               float* out, int64_t ldo, void* stream) {
+  if (!m || !l || N < 0) return MDN_EINVAL;
+  if (l->C != m->C) return MDN_ESHAPE;
+  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  if (l->device != m->device) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!A || !out || lda < m->D || ldo < l->M) return MDN_EINVAL;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  return cuda_status(
+      launch_amm_u8(m->trees(), l->dev(), A, N, lda, out, ldo, (cudaStream_t)stream));
 }
 
 int mdn_amm_variant(const mdn_model* m, const mdn_luts* l, int64_t lda, char* buf, size_t len) {

@@ -21,9 +21,11 @@ struct TreesDev {
   const uint16_t* dims;  // [C][4] global column of each level's split
   const float* thr;      // [C][16] heap order, pad slot 15 unused
   const uint16_t* sub;   // [C] first column of each codebook's subspace J^(c)
+  const uint16_t* q;     // [C][16] 8-bit split values ceil(v) in [0, 256] (uint8 input)
   int C;
   int D;
-  int subf;              // 1 / 2: every subspace is 16-B aligned and <= 4 / 8 wide
+  int subf;              // fp32: 1 / 2 = every subspace 16-B aligned and <= 4 / 8 wide
+  int subf_u8;           // uint8: 1 / 2 = every subspace exactly 4 / 8 bytes, contiguous
 };
 
 // Quantised tables as the kernels consume them (device).
@@ -43,6 +45,10 @@ cudaError_t launch_scan(const LutsDev& l, const uint8_t* codes, int64_t N, int32
                         float* out, int64_t ldo, cudaStream_t s);
 cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
                        int64_t lda, float* out, int64_t ldo, cudaStream_t s);
+cudaError_t launch_encode_u8(const TreesDev& t, const uint8_t* A, int64_t N, int64_t lda,
+                             uint8_t* codes, cudaStream_t s);
+cudaError_t launch_amm_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
+                          int64_t lda, float* out, int64_t ldo, cudaStream_t s);
 const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
                              const float* out, int64_t ldo);
 
@@ -72,12 +78,14 @@ struct mdn_model {
   std::vector<uint16_t> h_dims;   // [C][4]
   std::vector<float> h_thr;       // [C][16]
   std::vector<uint16_t> h_sub;    // [C] subspace begin
-  int subf = 0;
+  std::vector<uint16_t> h_q;      // [C][16] 8-bit split values
+  int subf = 0, subf_u8 = 0;
   uint16_t* d_dims = nullptr;
   float* d_thr = nullptr;
   uint16_t* d_sub = nullptr;
+  uint16_t* d_q = nullptr;
   float* d_P = nullptr;           // [16C][D]
-  mdn::TreesDev trees() const { return {d_dims, d_thr, d_sub, C, D, subf}; }
+  mdn::TreesDev trees() const { return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8}; }
 };
 
 struct mdn_luts {

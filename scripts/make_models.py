@@ -35,17 +35,20 @@ def main(names):
         t0 = time.time()
         n_test = 10000 if name in ("scale",) else min(spec.n_test, 200_000)
         A_train, A_test, B = make_config_data(name, n_test=n_test)
-        model = O.train(A_train, spec.C, lam=1.0, seed=spec.seed)
+        # 8-bit configs train on the pixel values as floats (the trees see the
+        # same numbers the u8 encoder compares against ceil(v), App. B reading R11)
+        model = O.train(A_train.astype(np.float32), spec.C, lam=1.0, seed=spec.seed)
         blob = O.write_model(model)
         with open(os.path.join(OUT, f"{name}.mdnm"), "wb") as f:
             f.write(blob)
         exact = A_test.astype(np.float64) @ B.astype(np.float64)
+        amm = O.amm_u8 if A_test.dtype == np.uint8 else O.amm
         rec = {"C": spec.C, "D": spec.D, "M": spec.M, "n_train": int(A_train.shape[0]),
                "sha256": hashlib.sha256(blob).hexdigest(), "bytes": len(blob),
                "train_s": round(time.time() - t0, 1), "nmse_rows": int(A_test.shape[0])}
         for mode in ("exact", "avg"):
             luts = O.make_luts(model, B, mode, spec.U)
-            _, _, out = O.amm(A_test, model, luts)
+            _, _, out = amm(A_test, model, luts)
             rec[f"nmse_{mode}"] = O.nmse(out, exact)
         manifest[name] = rec
         print(name, rec, flush=True)
