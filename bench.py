@@ -318,16 +318,18 @@ def run(args):
     # mix (read A, write M floats per row), timed the same way.
     probe = None
     if op == "amm" and not u8 and spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
+        probe_out = torch.empty_like(out)     # never overwrite the step's output
         for _ in range(2):
-            mdn.mdn_stream_probe(A, out, stream=stream)
+            mdn.mdn_stream_probe(A, probe_out, stream=stream)
         pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         torch.cuda.synchronize()
         pe[0].record(stream)
         for _ in range(args.steps):
-            mdn.mdn_stream_probe(A, out, stream=stream)
+            mdn.mdn_stream_probe(A, probe_out, stream=stream)
         pe[1].record(stream)
         torch.cuda.synchronize()
         t_probe = pe[0].elapsed_time(pe[1]) / 1e3 / args.steps
+        del probe_out
         probe = {"gbs": n * bytes_per_row / t_probe / 1e9,
                  "what": "plain streaming kernel, same bytes (read A, write M floats/row), no tables"}
     peak, peak_kind = _peaks()
