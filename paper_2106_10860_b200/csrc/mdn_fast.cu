@@ -33,6 +33,7 @@
 #include <mutex>
 
 #include "mdn_internal.h"
+#include "mdn_tma.cuh"
 
 namespace mdn {
 namespace fast {
@@ -73,58 +74,6 @@ struct Params {
   float* out;
   uint8_t* codes;                 // encode-only output
 };
-
-// ------------------------------------------------------------ PTX helpers --
-
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  uint32_t ok = 0;
-  const uint32_t a = su32(b);
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-// Optional L2 cache policy for the A tiles (Params::l2_hint; 0 = none, the
-// default: measured on cls100, evict_first costs 9% -- 2.45e9 vs 2.70e9 rows/s).
-__device__ __forceinline__ uint64_t l2_policy(int hint) {
-  uint64_t pol = 0;
-  if (hint == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  if (hint == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  if (hint == 3) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
-                                            uint64_t* bar, int hint, uint64_t policy) {
-  if (hint == 0) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
-        : "memory");
-  } else {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar)), "l"(policy)
-        : "memory");
-  }
-}
 
 // ------------------------------------------------------------ scan core --
 
@@ -523,11 +472,6 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-struct DevInfo {
-  int sms = 148;
-  int smem_optin = 232448;
-};
-
 DevInfo dev_info() {
   static DevInfo cache[16];
   static bool have[16] = {};
@@ -603,6 +547,11 @@ int env_int(const char* name, int dflt) {
 int knob_promo() {
   static int v = env_int("MDN_TMA_L2PROMO", 256);
   return v;
+}
+// MDN_NO_RT=1 disables the register-tree kernel (A/B comparisons only).
+bool rt_enabled() {
+  static int v = env_int("MDN_NO_RT", 0);
+  return v == 0;
 }
 int knob_hint() {
   static int v = env_int("MDN_TMA_HINT", 0);
@@ -708,6 +657,8 @@ static bool amm_fast_ok(const TreesDev& t, const LutsDev& l, const void* A, int6
 const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
                              const float* out, int64_t ldo) {
   Geometry g;
+  if (rt_enabled() && amm_rt_applies(t, l, 4))
+    return (l.M == 2 || l.M == 4) && ldo % l.M == 0 ? "rt_vec" : "rt";
   if (!amm_fast_ok(t, l, A, lda, 4, &g)) return "generic";
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
   static const char* names[2][3] = {{"ws_tma", "ws_tma_sub4", "ws_tma_sub8"},
@@ -801,15 +752,25 @@ static cudaError_t encode_fast(const TreesDev& t, const TIn* A, int64_t N, int64
 
 cudaError_t launch_amm(const TreesDev& t, const LutsDev& l, const float* A, int64_t N, int64_t lda,
                        float* out, int64_t ldo, cudaStream_t s) {
-  bool done;
-  cudaError_t e = amm_fast<float>(t, l, A, N, lda, out, ldo, s, &done);
+  bool done = false;
+  cudaError_t e;
+  if (rt_enabled()) {
+    e = launch_amm_rt(t, l, A, N, lda, out, ldo, s, &done);
+    if (done) return e;
+  }
+  e = amm_fast<float>(t, l, A, N, lda, out, ldo, s, &done);
   return done ? e : launch_amm_generic(t, l, A, 4, N, lda, out, ldo, s);
 }
 
 cudaError_t launch_amm_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
                           int64_t lda, float* out, int64_t ldo, cudaStream_t s) {
-  bool done;
-  cudaError_t e = amm_fast<uint8_t>(t, l, A, N, lda, out, ldo, s, &done);
+  bool done = false;
+  cudaError_t e;
+  if (rt_enabled()) {
+    e = launch_amm_rt_u8(t, l, A, N, lda, out, ldo, s, &done);
+    if (done) return e;
+  }
+  e = amm_fast<uint8_t>(t, l, A, N, lda, out, ldo, s, &done);
   return done ? e : launch_amm_generic(t, l, A, 1, N, lda, out, ldo, s);
 }
 

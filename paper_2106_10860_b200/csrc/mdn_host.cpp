@@ -245,6 +245,7 @@ void mdn_luts_free(mdn_luts* l) {
     DeviceGuard g(l->device);
     cudaFree(l->d_tq);
     cudaFree(l->d_words);
+    cudaFree(l->d_words16);
   }
   delete l;
 }
@@ -260,6 +261,11 @@ static int alloc_luts(int device, int C, int M, mdn_luts** out) {
   if ((st = dalloc(&l->d_tq, (size_t)C * K * M)) != MDN_OK) return st;
   if ((st = dalloc(&l->d_words, (size_t)C * l->W * K)) != MDN_OK) {
     cudaFree(l->d_tq);
+    return st;
+  }
+  if (M <= 2 * MAX_W2 && (st = dalloc(&l->d_words16, (size_t)C * K * ((M + 1) / 2))) != MDN_OK) {
+    cudaFree(l->d_tq);
+    cudaFree(l->d_words);
     return st;
   }
   *out = l.release();
@@ -297,7 +303,7 @@ int mdn_build_luts(const mdn_model* m, const float* B, int64_t M, int64_t ldb, i
   e = cudaMemcpy(dB, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = build_tables_dev(m->d_P, dB, C, D, (int)M, mode == MDN_SUM_AVG ? U : 0, dT, dDelta, dRange,
-                         dScal, l->d_tq, l->d_words, 0);
+                         dScal, l->d_tq, l->d_words, l->d_words16, 0);
   if (e == cudaSuccess) e = cudaMemcpy(&hs, dScal, sizeof(hs), cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) {
     l->delta.resize(C);
@@ -402,7 +408,7 @@ int mdn_luts_load(const void* buf, size_t len, int device, mdn_luts** out, size_
   l->model_fp = mfp;
   l->delta = delta;
   cudaError_t e = cudaMemcpy(l->d_tq, tqp, tq, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = pack_words_dev(l->d_tq, l->C, l->M, l->d_words, 0);
+  if (e == cudaSuccess) e = pack_words_dev(l->d_tq, l->C, l->M, l->d_words, l->d_words16, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     mdn_luts_free(l);

@@ -15,6 +15,7 @@ namespace mdn {
 constexpr int K = MDN_K;           // leaves per tree
 constexpr int THR_STRIDE = 16;     // 15 heap-ordered thresholds + 1 pad per codebook
 constexpr int MAX_C = 256;         // S <= 255 * C must fit the 16-bit SWAR lanes
+constexpr int MAX_W2 = 4;          // words16 tables are kept for M <= 8
 
 // Tree parameters as the kernels consume them (device).
 struct TreesDev {
@@ -32,6 +33,8 @@ struct TreesDev {
 struct LutsDev {
   const uint8_t* tq;     // canonical [C][16][M]
   const uint32_t* words; // scan layout [C][W][16]: word (c,w,k) = Tq[c][k][4w..4w+3]
+  const uint32_t* words16; // small-M scan layout [C][16][W2]: 2 columns per word in 16-bit
+                           // lanes (T[c][k][2w] | T[c][k][2w+1] << 16); null if M > 2*MAX_W2
   int C, M, W;
   int U;                 // 0 = exact sum; else averaging block size (power of two)
   float alpha_eff;       // alpha (exact) or alpha * U (avg): out = alpha_eff * S' + beta
@@ -49,6 +52,13 @@ cudaError_t launch_encode_u8(const TreesDev& t, const uint8_t* A, int64_t N, int
                              uint8_t* codes, cudaStream_t s);
 cudaError_t launch_amm_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
                           int64_t lda, float* out, int64_t ldo, cudaStream_t s);
+// Register-tree kernel for C <= 8, M <= 4 (mdn_small.cu); *done = false when
+// the shapes are not covered (the caller then uses the general kernels).
+cudaError_t launch_amm_rt(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
+                          int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done);
+cudaError_t launch_amm_rt_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
+                             int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done);
+bool amm_rt_applies(const TreesDev& t, const LutsDev& l, int es);
 const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
                              const float* out, int64_t ldo);
 
@@ -62,8 +72,9 @@ struct LutScalars {
 cudaError_t build_tables_dev(const float* dP, const float* dB, int C, int D, int M,
                              int U_or_0, double* dT, double* dDelta, double* dRange,
                              LutScalars* dScal, uint8_t* dTq, uint32_t* dWords,
-                             cudaStream_t s);
-cudaError_t pack_words_dev(const uint8_t* dTq, int C, int M, uint32_t* dWords, cudaStream_t s);
+                             uint32_t* dWords16, cudaStream_t s);
+cudaError_t pack_words_dev(const uint8_t* dTq, int C, int M, uint32_t* dWords,
+                           uint32_t* dWords16, cudaStream_t s);
 
 uint64_t fnv1a64(const uint8_t* p, size_t n);
 
@@ -96,8 +107,9 @@ struct mdn_luts {
   std::vector<double> delta;
   uint8_t* d_tq = nullptr;       // [C][16][M]
   uint32_t* d_words = nullptr;   // [C][W][16]
+  uint32_t* d_words16 = nullptr; // [C][16][W2], M <= 2 * MAX_W2 only
   mdn::LutsDev dev() const {
     float ae = mode == MDN_SUM_AVG ? alpha * (float)U : alpha;   // exact: power of two
-    return {d_tq, d_words, C, M, W, mode == MDN_SUM_AVG ? U : 0, ae, beta32};
+    return {d_tq, d_words, d_words16, C, M, W, mode == MDN_SUM_AVG ? U : 0, ae, beta32};
   }
 };

@@ -114,17 +114,41 @@ __global__ void k_pack_words(const uint8_t* __restrict__ tq, int C, int M,
   words[i] = v;
 }
 
+// Small-M scan layout (mdn_small.cu): words16[(c*16 + k)*W2 + w] =
+// Tq[c][k][2w] | Tq[c][k][2w+1] << 16 (zero beyond M). Exact sums of up to
+// 257 such words cannot carry across the 16-bit lanes (255 C < 2^16).
+__global__ void k_pack_words16(const uint8_t* __restrict__ tq, int C, int M,
+                               uint32_t* __restrict__ words16) {
+  const int W2 = (M + 1) / 2;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)C * K * W2) return;
+  const int w = (int)(i % W2);
+  const int64_t ck = i / W2;                       // c * 16 + k
+  uint32_t v = 0;
+  for (int b = 0; b < 2; ++b) {
+    int m = 2 * w + b;
+    uint32_t byte = m < M ? tq[ck * M + m] : 0u;
+    v |= byte << (16 * b);
+  }
+  words16[i] = v;
+}
+
 }  // namespace
 
-cudaError_t pack_words_dev(const uint8_t* dTq, int C, int M, uint32_t* dWords, cudaStream_t s) {
+cudaError_t pack_words_dev(const uint8_t* dTq, int C, int M, uint32_t* dWords,
+                           uint32_t* dWords16, cudaStream_t s) {
   int64_t n = (int64_t)C * ((M + 3) / 4) * K;
   k_pack_words<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dTq, C, M, dWords);
+  if (dWords16) {
+    int64_t n16 = (int64_t)C * K * ((M + 1) / 2);
+    k_pack_words16<<<(unsigned)((n16 + 255) / 256), 256, 0, s>>>(dTq, C, M, dWords16);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t build_tables_dev(const float* dP, const float* dB, int C, int D, int M, int U_or_0,
                              double* dT, double* dDelta, double* dRange, LutScalars* dScal,
-                             uint8_t* dTq, uint32_t* dWords, cudaStream_t s) {
+                             uint8_t* dTq, uint32_t* dWords, uint32_t* dWords16, cudaStream_t s) {
   const int KC = K * C;
   int64_t n = (int64_t)KC * M;
   k_tables<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(dP, dB, KC, D, M, dT);
@@ -133,7 +157,7 @@ cudaError_t build_tables_dev(const float* dP, const float* dB, int C, int D, int
   k_quant<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dT, dDelta, M, n, dScal, dTq);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  e = pack_words_dev(dTq, C, M, dWords, s);
+  e = pack_words_dev(dTq, C, M, dWords, dWords16, s);
   if (e != cudaSuccess) return e;
   return cudaStreamSynchronize(s);
 }

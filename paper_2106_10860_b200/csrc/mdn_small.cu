@@ -1,0 +1,383 @@
+// Register-tree kernel for the small-row MADDNESS configurations (C <= 8
+// codebooks, M <= 4 output columns: the Tiny and image-filter workloads, and
+// the 8-bit image path of SURVEY N1).
+//
+// With rows of 32 values the fused path must sustain 4-16e10 rows/s, i.e. a
+// budget of roughly 200 thread-instructions per row at full issue, and the
+// general kernel (mdn_fast.cu: thread per row, thresholds gathered from shared
+// memory at every level, 4 output columns per table word) spends ~480 on the
+// 8-bit image rows. This kernel is organised so that nothing per-codebook is
+// looked up at run time:
+//
+//   warp 0        TMA producer: one 2-D box of R = 256 rows per stage into an
+//                 NS-deep shared-memory ring (mbarrier complete_tx).
+//   warps 1..NWK  workers, in NG groups of 8; group g takes every NG-th stage
+//                 and warp k of the group its rows [32k, 32k + 32):
+//     encode      lane -> (row lane / C, codebook lane % C), C iterations per
+//                 32 rows. Each lane owns ONE codebook for the whole kernel,
+//                 so its tree -- 15 thresholds and 4 split
+//                 dims -- lives in registers. Algorithm 1 (L228-248) becomes
+//                 4 compares and 11 selects (the threshold of level t is picked
+//                 by the bits already decided, L239), no shared gathers.
+//                 8-bit rows: the codebook's 4-byte subspace is one 32-bit
+//                 shared load and each split value one PRMT (App. B split
+//                 values q = ceil(v), reading R11).
+//     hand-off    the code (pre-scaled to a table byte offset) goes to a
+//                 warp-private shared buffer; __syncwarp.
+//     scan        lane -> row. Tables are the 16-bit-lane layout
+//                 words16[c][k][w] = T[c][k][2w] | T[c][k][2w+1] << 16, so an
+//                 exact sum is ONE add per (row, codebook, 2 columns), and an
+//                 App. D average mu(a,b) = (a+b+1) >> 1 is 3 ops per 2 columns
+//                 (vs 5 for __vavgu4 on 4 byte lanes).
+//     dequant     out = fl32(alpha_eff * S + beta32) (Eq. 1), S -> fp32
+//                 by the 2^23 magic-number trick (exact for S < 2^23), one
+//                 FFMA rounding; 8- or 16-byte stores.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "mdn_internal.h"
+#include "mdn_tma.cuh"
+
+namespace mdn {
+namespace fast {
+namespace small {
+
+constexpr int R = 256;                   // rows per stage (= TMA box rows)
+constexpr int CPS = R / 32;              // 32-row chunks per stage = warps per group
+constexpr int NG = 2;                    // worker groups
+constexpr int NWK = NG * CPS;            // worker warps
+constexpr int THREADS = 32 * (1 + NWK);
+constexpr int NS_MAX = 8;
+
+struct SParams {
+  int64_t N, n_tiles, ldo;
+  int pitch_e;                   // elements per shared row (D + 16 bytes of padding)
+  int stage_b;                   // bytes per stage, 128-aligned
+  int NS;
+  int M;
+  float alpha_eff, beta32;
+  const uint32_t* lut16;         // global [C][16][W2]
+  const uint16_t* dims;          // global [C][4]
+  const uint16_t* sub;           // global [C]
+  const float* thr;              // global [C][16]
+  const uint16_t* q;             // global [C][16]
+  float* out;
+};
+
+// Code-row stride in words: 16-B aligned and conflict-free for the lane-per-row
+// LDS.128 reads (C = 8: 48-B rows spread a quarter-warp over all 32 banks).
+template <int C>
+struct CodeStride {
+  static constexpr int value = C == 8 ? 12 : 4;
+};
+
+// Algorithm 1 with the tree in registers: p <- 2p + [x_t >= v^t_p] where the
+// level-t threshold v^t_p is selected by the bits b_0..b_{t-1} already taken.
+template <class V>
+__device__ __forceinline__ uint32_t tree_code(V x0, V x1, V x2, V x3, const V (&t)[15]) {
+  const bool b0 = x0 >= t[0];
+  const bool b1 = x1 >= (b0 ? t[2] : t[1]);
+  const V u2 = b0 ? (b1 ? t[6] : t[5]) : (b1 ? t[4] : t[3]);
+  const bool b2 = x2 >= u2;
+  const V e0 = b2 ? t[8] : t[7], e1 = b2 ? t[10] : t[9];
+  const V e2 = b2 ? t[12] : t[11], e3 = b2 ? t[14] : t[13];
+  const V u3 = b0 ? (b1 ? e3 : e2) : (b1 ? e1 : e0);
+  const bool b3 = x3 >= u3;
+  return (b0 ? 8u : 0u) + (b1 ? 4u : 0u) + (b2 ? 2u : 0u) + (b3 ? 1u : 0u);
+}
+
+// mu(a, b) = floor((a + b + 1) / 2) on two 16-bit lanes holding values < 256
+// (App. D): the sum is < 512, so no carry crosses lanes; the shift moves
+// the high lane's bit 0 into bit 15, which the mask clears.
+__device__ __forceinline__ uint32_t avg16(uint32_t a, uint32_t b) {
+  return ((a + b + 0x00010001u) >> 1) & 0x7FFF7FFFu;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ float u16_to_f(uint32_t s) {
+  return __uint_as_float(0x4B000000u | s) - 8388608.0f;   // exact for s < 2^23
+}
+
+// TIn = float: fp32 rows. TIn = uint8_t: 8-bit rows whose codebooks are
+// 4-byte subspaces [4c, 4c + 4) (the image config; other byte layouts use the
+// general kernel). VEC: 0 = guarded scalar stores, 1 = M == 2 W2 with 8-byte
+// (W2 odd) or 16-byte (W2 even) aligned rows.
+template <class TIn, int D, int C, int W2, int U, int VEC>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_amm_rt(const __grid_constant__ CUtensorMap tmap, const SParams p) {
+  constexpr int PITCH = D + 16 / (int)sizeof(TIn);  // shared row pitch (elements)
+  constexpr int RPW = 32 / C;                       // rows per encode iteration
+  constexpr int CS = CodeStride<C>::value;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + NS_MAX;
+  constexpr int OFF_LUT = 256;
+  constexpr int OFF_CODE = OFF_LUT + C * 16 * W2 * 4;
+  constexpr int OFF_STAGE = (OFF_CODE + NWK * 32 * CS * 4 + 127) & ~127;
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  for (int i = tid; i < C * 16 * W2; i += blockDim.x) s_lut[i] = p.lut16[i];
+  if (tid == 0) {
+    for (int s = 0; s < p.NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  __syncthreads();
+
+  // Local stage sequence of this CTA: tiles blockIdx.x, blockIdx.x + grid, ...
+  const int64_t n_local = (p.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(R * p.pitch_e * sizeof(TIn));
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t q = 0; q < n_local; ++q) {
+        mbar_wait_sleep(&empty[s], ph ^ 1u);
+        mbar_arrive_tx(&full[s], bytes);
+        const int64_t y = (blockIdx.x + q * gridDim.x) * (int64_t)R;
+        tma_load_2d(smem + OFF_STAGE + (size_t)s * p.stage_b, &tmap, 0, (int)y, &full[s], 0, 0);
+        if (++s == p.NS) s = 0, ph ^= 1u;
+      }
+    }
+    return;
+  }
+
+  // ---------------- workers ----------------
+  const int wk = warp - 1;
+  const int grp = wk / CPS, chunk = wk % CPS;
+  const int c = lane % C;                            // this lane's codebook (fixed)
+  const int rs = lane / C;
+  uint32_t* s_code = reinterpret_cast<uint32_t*>(smem + OFF_CODE) + wk * 32 * CS;
+
+  // The lane's tree in registers.
+  using V = typename std::conditional<sizeof(TIn) == 1, int, float>::type;
+  V th[15];
+#pragma unroll
+  for (int i = 0; i < 15; ++i) {
+    if constexpr (sizeof(TIn) == 1) th[i] = (int)p.q[c * 16 + i];
+    else th[i] = p.thr[c * 16 + i];
+  }
+  int o[4];                                          // split-dim element offsets
+  uint32_t sel[4];                                   // 8-bit rows: PRMT selectors
+  const int sub = p.sub[c];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    o[t] = p.dims[c * 4 + t];
+    sel[t] = (uint32_t)(o[t] - sub) | 0x4440u;       // zero-extend the selected byte
+  }
+
+  // Per-lane addressing, fixed for the kernel: the lane reads row rs of each
+  // RPW-row group; the codebook's table base (absolute shared address) is
+  // folded into the stored code so the scanner's lookups need no adds.
+  const uint32_t lut_c = su32(s_lut) + (uint32_t)(c * 16 * W2 * 4);
+  int s = grp, ph = 0;
+  while (s >= p.NS) s -= p.NS, ph ^= 1;
+  for (int64_t q = grp; q < n_local; q += NG) {
+    mbar_wait_sleep(&full[s], (uint32_t)ph);
+    const TIn* stg = reinterpret_cast<const TIn*>(smem + OFF_STAGE + (size_t)s * p.stage_b) +
+                     (size_t)(chunk * 32 + rs) * PITCH;
+    // ---- encode 32 rows: C iterations of RPW rows x C codebooks ----
+    // All loads first, then the (independent) trees, then the stores, so the
+    // compiler may interleave the C dependency chains.
+    uint32_t code[C];
+    if constexpr (sizeof(TIn) == 1) {
+      uint32_t w[C];
+#pragma unroll
+      for (int it = 0; it < C; ++it)
+        w[it] = *reinterpret_cast<const uint32_t*>(stg + it * RPW * PITCH + sub);
+#pragma unroll
+      for (int it = 0; it < C; ++it)
+        code[it] = tree_code<int>((int)__byte_perm(w[it], 0u, sel[0]), (int)__byte_perm(w[it], 0u, sel[1]),
+                                  (int)__byte_perm(w[it], 0u, sel[2]), (int)__byte_perm(w[it], 0u, sel[3]), th);
+    } else {
+      float x[C][4];
+#pragma unroll
+      for (int it = 0; it < C; ++it)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) x[it][t] = stg[it * RPW * PITCH + o[t]];
+#pragma unroll
+      for (int it = 0; it < C; ++it) code[it] = tree_code<float>(x[it][0], x[it][1], x[it][2], x[it][3], th);
+    }
+#pragma unroll
+    for (int it = 0; it < C; ++it)
+      s_code[(it * RPW + rs) * CS + c] = lut_c + code[it] * (4u * W2);   // table entry address
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);           // this chunk's rows are consumed
+    // ---- scan row `lane` ----
+    uint32_t off[C];
+#pragma unroll
+    for (int k = 0; k < C; k += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(s_code + lane * CS + k);
+      off[k] = v.x, off[k + 1] = v.y, off[k + 2] = v.z, off[k + 3] = v.w;
+    }
+    __syncwarp();                                    // s_code may be rewritten next stage
+    uint32_t acc[W2];
+#pragma unroll
+    for (int w = 0; w < W2; ++w) acc[w] = 0u;
+    if constexpr (U == 0) {
+#pragma unroll
+      for (int cc = 0; cc < C; ++cc)
+#pragma unroll
+        for (int w = 0; w < W2; ++w)
+          acc[w] += lds_u32(off[cc] + 4 * w);
+    } else {
+      static_assert((U & (U - 1)) == 0 && C % U == 0, "U must be a power of two dividing C");
+#pragma unroll
+      for (int blk = 0; blk < C / U; ++blk)
+#pragma unroll
+        for (int w = 0; w < W2; ++w) {
+          uint32_t v[U];
+#pragma unroll
+          for (int i = 0; i < U; ++i) {
+            const int cc = blk * U + i;
+            v[i] = lds_u32(off[cc] + 4 * w);
+          }
+#pragma unroll
+          for (int st = 1; st < U; st *= 2)          // halves recursion = adjacent pairs (R17)
+#pragma unroll
+            for (int i = 0; i < U; i += 2 * st) v[i] = avg16(v[i], v[i + st]);
+          acc[w] += v[0];
+        }
+    }
+    const int64_t row = (blockIdx.x + q * gridDim.x) * (int64_t)R + chunk * 32 + lane;
+    if (row < p.N) {
+      float* o_row = p.out + row * p.ldo;
+      float f[2 * W2];
+#pragma unroll
+      for (int w = 0; w < W2; ++w) {
+        f[2 * w] = __fmaf_rn(p.alpha_eff, u16_to_f(acc[w] & 0xFFFFu), p.beta32);
+        f[2 * w + 1] = __fmaf_rn(p.alpha_eff, u16_to_f(acc[w] >> 16), p.beta32);
+      }
+      if constexpr (VEC) {
+        if constexpr (W2 % 2 == 0) {
+#pragma unroll
+          for (int w = 0; w < W2; w += 2)
+            *reinterpret_cast<float4*>(o_row + 2 * w) = make_float4(f[2 * w], f[2 * w + 1], f[2 * w + 2], f[2 * w + 3]);
+        } else {
+#pragma unroll
+          for (int w = 0; w < W2; ++w)
+            *reinterpret_cast<float2*>(o_row + 2 * w) = make_float2(f[2 * w], f[2 * w + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 2 * W2; ++m)
+          if (m < p.M) o_row[m] = f[m];
+      }
+    }
+    s += NG;
+    while (s >= p.NS) s -= p.NS, ph ^= 1;
+  }
+}
+
+template <class TIn, int C, int W2, int U, int VEC>
+cudaError_t launch(const CUtensorMap& tm, const SParams& p, size_t smem, cudaStream_t st) {
+  auto k = k_amm_rt<TIn, 32, C, W2, U, VEC>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
+  k<<<(unsigned)grid, THREADS, smem, st>>>(tm, p);
+  return cudaGetLastError();
+}
+
+template <class TIn, int C, int W2, int U>
+cudaError_t launch_v(const CUtensorMap& tm, const SParams& p, size_t smem, bool vec, cudaStream_t st) {
+  return vec ? launch<TIn, C, W2, U, 1>(tm, p, smem, st) : launch<TIn, C, W2, U, 0>(tm, p, smem, st);
+}
+
+}  // namespace small
+}  // namespace fast
+
+using namespace fast;
+using namespace fast::small;
+
+// Is the register-tree kernel applicable? C in {4, 8}, M <= 4, U in {0, C},
+// the padded row fits one TMA box, 16-B aligned A; 8-bit rows additionally need
+// 4-byte subspaces [4c, 4c + 4) (t.subf_u8 == 1).
+static bool rt_ok(const TreesDev& t, const LutsDev& l, const void* A, int64_t lda, int es) {
+  if (!(t.C == 4 || t.C == 8) || l.M > 4 || !l.words16) return false;
+  if (!(l.U == 0 || l.U == t.C)) return false;
+  if ((reinterpret_cast<uintptr_t>(A) & 15u) || (lda * es) % 16) return false;
+  if (t.D != 32) return false;                     // compiled row width (Tiny / image configs)
+  if (es == 1 && t.subf_u8 != 1) return false;
+  return true;
+}
+
+template <class TIn>
+static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int64_t N,
+                          int64_t lda, float* out, int64_t ldo, cudaStream_t st, bool* done) {
+  constexpr int es = sizeof(TIn);
+  *done = false;
+  if (N > (int64_t)0x7FFFFF00 || !rt_ok(t, l, A, lda, es)) return cudaSuccess;
+  const int pitch_e = t.D + 16 / es;
+  const int stage_b = ((R * pitch_e * es) + 127) & ~127;
+  const int W2 = (l.M + 1) / 2;
+  const size_t fixed = ((256 + (size_t)t.C * 16 * W2 * 4 + (size_t)NWK * 32 * (t.C == 8 ? 12 : 4) * 4) + 127) & ~size_t(127);
+  const size_t budget = (size_t)dev_info().smem_optin;
+  if (fixed + (size_t)2 * NG * stage_b > budget) return cudaSuccess;
+  int NS = (int)((budget - fixed) / stage_b);
+  if (NS > NS_MAX) NS = NS_MAX;
+  // Each worker group must own its ring slots (NS % NG == 0): a slot shared by
+  // two groups could be waited on for phase k+1 by one group while phase k is
+  // still incomplete, which the parity wait cannot tell apart.
+  NS -= NS % NG;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, A, N, lda, t.D, t.D, R, es)) return cudaSuccess;
+  SParams p{};
+  p.N = N;
+  p.n_tiles = (N + R - 1) / R;
+  p.ldo = ldo;
+  p.pitch_e = pitch_e;
+  p.stage_b = stage_b;
+  p.NS = NS;
+  p.M = l.M;
+  p.alpha_eff = l.alpha_eff;
+  p.beta32 = l.beta32;
+  p.lut16 = l.words16;
+  p.dims = t.dims;
+  p.sub = t.sub;
+  p.thr = t.thr;
+  p.q = t.q;
+  p.out = out;
+  const size_t smem = fixed + (size_t)NS * stage_b;
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
+  const bool vec = l.M == 2 * W2 &&
+                   (W2 % 2 == 0 ? (ldo % 4 == 0 && (oa & 15u) == 0) : (ldo % 2 == 0 && (oa & 7u) == 0));
+  *done = true;
+  const bool avg = l.U != 0;
+  if (t.C == 4 && W2 == 1) return avg ? launch_v<TIn, 4, 1, 4>(tm, p, smem, vec, st) : launch_v<TIn, 4, 1, 0>(tm, p, smem, vec, st);
+  if (t.C == 4 && W2 == 2) return avg ? launch_v<TIn, 4, 2, 4>(tm, p, smem, vec, st) : launch_v<TIn, 4, 2, 0>(tm, p, smem, vec, st);
+  if (t.C == 8 && W2 == 1) return avg ? launch_v<TIn, 8, 1, 8>(tm, p, smem, vec, st) : launch_v<TIn, 8, 1, 0>(tm, p, smem, vec, st);
+  if (t.C == 8 && W2 == 2) return avg ? launch_v<TIn, 8, 2, 8>(tm, p, smem, vec, st) : launch_v<TIn, 8, 2, 0>(tm, p, smem, vec, st);
+  *done = false;
+  return cudaSuccess;
+}
+
+cudaError_t launch_amm_rt(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
+                          int64_t lda, float* out, int64_t ldo, cudaStream_t st, bool* done) {
+  return amm_rt<float>(t, l, A, N, lda, out, ldo, st, done);
+}
+
+cudaError_t launch_amm_rt_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
+                             int64_t lda, float* out, int64_t ldo, cudaStream_t st, bool* done) {
+  return amm_rt<uint8_t>(t, l, A, N, lda, out, ldo, st, done);
+}
+
+bool amm_rt_applies(const TreesDev& t, const LutsDev& l, int es) {
+  return rt_ok(t, l, reinterpret_cast<const void*>(256), t.D, es);
+}
+
+}  // namespace mdn
