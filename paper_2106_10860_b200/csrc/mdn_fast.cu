@@ -553,6 +553,11 @@ bool rt_enabled() {
   static int v = env_int("MDN_NO_RT", 0);
   return v == 0;
 }
+// MDN_NO_BQ=1 disables the byte-threshold encoder of the 8-bit path (A/B only).
+bool knob_bq() {
+  static int v = env_int("MDN_NO_BQ", 0);
+  return v == 0;
+}
 int knob_hint() {
   static int v = env_int("MDN_TMA_HINT", 0);
   return v;

@@ -192,6 +192,9 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
     double q = std::ceil((double)m->h_thr[i]);
     m->h_q[i] = (uint16_t)(q < 0 ? 0 : (q > 256 ? 256 : q));
   }
+  m->q_byte = 1;
+  for (uint32_t cc = 0; cc < C; ++cc)
+    for (int i = 0; i < 15; ++i) m->q_byte &= m->h_q[cc * THR_STRIDE + i] <= 255 ? 1 : 0;
   size_t p_bytes = (size_t)K * C * D * sizeof(float);
   if (!r.need(p_bytes + 8)) return set_err(err_off, r.fail_off, MDN_EFORMAT);
   const uint8_t* P = r.p + r.off;

@@ -27,6 +27,7 @@ struct TreesDev {
   int D;
   int subf;              // fp32: 1 / 2 = every subspace 16-B aligned and <= 4 / 8 wide
   int subf_u8;           // uint8: 1 / 2 = every subspace exactly 4 / 8 bytes, contiguous
+  int q_byte;            // every 8-bit split value q <= 255 (fits a byte)
 };
 
 // Quantised tables as the kernels consume them (device).
@@ -90,13 +91,13 @@ struct mdn_model {
   std::vector<float> h_thr;       // [C][16]
   std::vector<uint16_t> h_sub;    // [C] subspace begin
   std::vector<uint16_t> h_q;      // [C][16] 8-bit split values
-  int subf = 0, subf_u8 = 0;
+  int subf = 0, subf_u8 = 0, q_byte = 0;
   uint16_t* d_dims = nullptr;
   float* d_thr = nullptr;
   uint16_t* d_sub = nullptr;
   uint16_t* d_q = nullptr;
   float* d_P = nullptr;           // [16C][D]
-  mdn::TreesDev trees() const { return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8}; }
+  mdn::TreesDev trees() const { return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8, q_byte}; }
 };
 
 struct mdn_luts {

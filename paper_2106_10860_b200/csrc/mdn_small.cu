@@ -88,6 +88,53 @@ __device__ __forceinline__ uint32_t tree_code(V x0, V x1, V x2, V x3, const V (&
   return (b0 ? 8u : 0u) + (b1 ? 4u : 0u) + (b2 ? 2u : 0u) + (b3 ? 1u : 0u);
 }
 
+// 8-bit rows whose split values all fit a byte (q <= 255; always true for a
+// model trained on 8-bit data, App. B): Algorithm 1 with one byte-shuffle per
+// level instead of a select tree, and the rest as adds / multiplies so that
+// ptxas can spread the work over the FMA pipe as well as the ALU pipe (the
+// select-tree version saturates the ALU pipe at 85% on the image_u8 config).
+//   lt_t = [x_t < v_t] = 1 - b_t is the sign bit of x_t - v_t;
+//   n_{t+1} = 2 n_t + lt_t is the complemented node index (n_4 = 15 - code).
+//   Levels 2 and 3 pick their threshold with PRMT from the byte-packed level
+//   table (complemented node order), selector n * 0x11: bytes 0 and 1 hold the
+//   threshold, bytes 2 and 3 byte 0 of the table (g); the split value is
+//   packed the same way (x, x, g, g), so the word difference is (x - v) * 257
+//   and its sign is the compare.
+struct ByteTree {
+  int q0, q2, d12;                 // level 0 threshold; level 1: v = q2 + lt0 * (q1 - q2)
+  uint32_t Q2, Q3lo, Q3hi;         // level tables, byte n = threshold of complemented node n
+  uint32_t s0, s1, s2, s3;         // PRMT selectors of the split values in the subspace word
+  uint32_t g2, g3;                 // byte 0 of Q2 / Q3lo (pad bytes of the packed compares)
+  uint32_t base;                   // table address of code 15 (n_4 = 0)
+};
+
+// Raw PRMT / shift: __byte_perm masks its selector (LOP3 & 0x7777) to hide
+// PRMT's sign-replicate bit, and a plain (x - v) >> 31 is pattern-matched back
+// into ISETP + SEL (ALU pipe); our selectors never set bit 3 of a nibble.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+__device__ __forceinline__ uint32_t sign_bit(uint32_t x) {
+  uint32_t d;
+  asm("shr.u32 %0, %1, 31;" : "=r"(d) : "r"(x));
+  return d;
+}
+
+template <int W2>
+__device__ __forceinline__ uint32_t byte_tree_addr(uint32_t w, const ByteTree& b) {
+  const uint32_t lt0 = sign_bit(prmt(w, 0u, b.s0) - (uint32_t)b.q0);
+  const uint32_t v1 = (uint32_t)b.q2 + lt0 * (uint32_t)b.d12;
+  const uint32_t lt1 = sign_bit(prmt(w, 0u, b.s1) - v1);
+  const uint32_t n2 = 2u * lt0 + lt1;
+  const uint32_t lt2 = sign_bit(prmt(w, b.g2, b.s2) - prmt(b.Q2, b.Q2, n2 * 0x11u));
+  const uint32_t n3 = 2u * n2 + lt2;
+  const uint32_t lt3 = sign_bit(prmt(w, b.g3, b.s3) - prmt(b.Q3lo, b.Q3hi, n3 * 0x11u));
+  const uint32_t n4 = 2u * n3 + lt3;               // 15 - code
+  return b.base - n4 * (4u * W2);
+}
+
 // mu(a, b) = floor((a + b + 1) / 2) on two 16-bit lanes holding values < 256
 // (App. D): the sum is < 512, so no carry crosses lanes; the shift moves
 // the high lane's bit 0 into bit 15, which the mask clears.
@@ -109,7 +156,7 @@ __device__ __forceinline__ float u16_to_f(uint32_t s) {
 // 4-byte subspaces [4c, 4c + 4) (the image config; other byte layouts use the
 // general kernel). VEC: 0 = guarded scalar stores, 1 = M == 2 W2 with 8-byte
 // (W2 odd) or 16-byte (W2 even) aligned rows.
-template <class TIn, int D, int C, int W2, int U, int VEC>
+template <class TIn, int D, int C, int W2, int U, int VEC, bool BQ>
 __global__ void __launch_bounds__(THREADS, 1)
     k_amm_rt(const __grid_constant__ CUtensorMap tmap, const SParams p) {
   constexpr int PITCH = D + 16 / (int)sizeof(TIn);  // shared row pitch (elements)
@@ -184,25 +231,57 @@ __global__ void __launch_bounds__(THREADS, 1)
   // RPW-row group; the codebook's table base (absolute shared address) is
   // folded into the stored code so the scanner's lookups need no adds.
   const uint32_t lut_c = su32(s_lut) + (uint32_t)(c * 16 * W2 * 4);
+  ByteTree bt{};
+  if constexpr (BQ) {
+    const uint16_t* qc = p.q + c * 16;             // heap order; complemented node n at level t
+    bt.q0 = qc[0];                                 //   is heap index 2^(t+1) - 2 - n
+    bt.q2 = qc[2];
+    bt.d12 = (int)qc[1] - (int)qc[2];
+    bt.Q2 = 0u, bt.Q3lo = 0u, bt.Q3hi = 0u;
+#pragma unroll
+    for (int n = 0; n < 4; ++n) bt.Q2 |= (uint32_t)qc[6 - n] << (8 * n);
+#pragma unroll
+    for (int n = 0; n < 4; ++n) bt.Q3lo |= (uint32_t)qc[14 - n] << (8 * n);
+#pragma unroll
+    for (int n = 0; n < 4; ++n) bt.Q3hi |= (uint32_t)qc[10 - n] << (8 * n);
+    bt.g2 = bt.Q2 & 0xFFu;
+    bt.g3 = bt.Q3lo & 0xFFu;
+    const uint32_t j0 = o[0] - sub, j1 = o[1] - sub, j2 = o[2] - sub, j3 = o[3] - sub;
+    bt.s0 = j0 | 0x4440u;
+    bt.s1 = j1 | 0x4440u;
+    bt.s2 = j2 | (j2 << 4) | 0x4400u;
+    bt.s3 = j3 | (j3 << 4) | 0x4400u;
+    bt.base = lut_c + 15u * 4u * W2;
+  }
   int s = grp, ph = 0;
   while (s >= p.NS) s -= p.NS, ph ^= 1;
-  for (int64_t q = grp; q < n_local; q += NG) {
+  // This lane's output row and pointer, advanced by a constant stride per stage.
+  int64_t row = ((int64_t)blockIdx.x + (int64_t)grp * gridDim.x) * R + chunk * 32 + lane;
+  const int64_t row_step = (int64_t)NG * gridDim.x * R;
+  float* o_row = p.out + row * p.ldo;
+  const int64_t o_step = row_step * p.ldo;
+  for (int64_t q = grp; q < n_local; q += NG, row += row_step, o_row += o_step) {
     mbar_wait_sleep(&full[s], (uint32_t)ph);
     const TIn* stg = reinterpret_cast<const TIn*>(smem + OFF_STAGE + (size_t)s * p.stage_b) +
                      (size_t)(chunk * 32 + rs) * PITCH;
     // ---- encode 32 rows: C iterations of RPW rows x C codebooks ----
     // All loads first, then the (independent) trees, then the stores, so the
     // compiler may interleave the C dependency chains.
-    uint32_t code[C];
+    uint32_t code[C];                                // table entry addresses
     if constexpr (sizeof(TIn) == 1) {
       uint32_t w[C];
 #pragma unroll
       for (int it = 0; it < C; ++it)
         w[it] = *reinterpret_cast<const uint32_t*>(stg + it * RPW * PITCH + sub);
 #pragma unroll
-      for (int it = 0; it < C; ++it)
-        code[it] = tree_code<int>((int)__byte_perm(w[it], 0u, sel[0]), (int)__byte_perm(w[it], 0u, sel[1]),
-                                  (int)__byte_perm(w[it], 0u, sel[2]), (int)__byte_perm(w[it], 0u, sel[3]), th);
+      for (int it = 0; it < C; ++it) {
+        if constexpr (BQ)
+          code[it] = byte_tree_addr<W2>(w[it], bt);
+        else
+          code[it] = lut_c + 4u * W2 *
+                     tree_code<int>((int)__byte_perm(w[it], 0u, sel[0]), (int)__byte_perm(w[it], 0u, sel[1]),
+                                    (int)__byte_perm(w[it], 0u, sel[2]), (int)__byte_perm(w[it], 0u, sel[3]), th);
+      }
     } else {
       float x[C][4];
 #pragma unroll
@@ -210,11 +289,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int t = 0; t < 4; ++t) x[it][t] = stg[it * RPW * PITCH + o[t]];
 #pragma unroll
-      for (int it = 0; it < C; ++it) code[it] = tree_code<float>(x[it][0], x[it][1], x[it][2], x[it][3], th);
+      for (int it = 0; it < C; ++it)
+        code[it] = lut_c + 4u * W2 * tree_code<float>(x[it][0], x[it][1], x[it][2], x[it][3], th);
     }
 #pragma unroll
-    for (int it = 0; it < C; ++it)
-      s_code[(it * RPW + rs) * CS + c] = lut_c + code[it] * (4u * W2);   // table entry address
+    for (int it = 0; it < C; ++it) s_code[(it * RPW + rs) * CS + c] = code[it];
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);           // this chunk's rows are consumed
     // ---- scan row `lane` ----
@@ -253,9 +332,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           acc[w] += v[0];
         }
     }
-    const int64_t row = (blockIdx.x + q * gridDim.x) * (int64_t)R + chunk * 32 + lane;
     if (row < p.N) {
-      float* o_row = p.out + row * p.ldo;
       float f[2 * W2];
 #pragma unroll
       for (int w = 0; w < W2; ++w) {
@@ -283,9 +360,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <class TIn, int C, int W2, int U, int VEC>
+template <class TIn, int C, int W2, int U, int VEC, bool BQ>
 cudaError_t launch(const CUtensorMap& tm, const SParams& p, size_t smem, cudaStream_t st) {
-  auto k = k_amm_rt<TIn, 32, C, W2, U, VEC>;
+  auto k = k_amm_rt<TIn, 32, C, W2, U, VEC, BQ>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
@@ -294,8 +371,15 @@ cudaError_t launch(const CUtensorMap& tm, const SParams& p, size_t smem, cudaStr
 }
 
 template <class TIn, int C, int W2, int U>
-cudaError_t launch_v(const CUtensorMap& tm, const SParams& p, size_t smem, bool vec, cudaStream_t st) {
-  return vec ? launch<TIn, C, W2, U, 1>(tm, p, smem, st) : launch<TIn, C, W2, U, 0>(tm, p, smem, st);
+cudaError_t launch_v(const CUtensorMap& tm, const SParams& p, size_t smem, bool vec, bool bq,
+                     cudaStream_t st) {
+  if constexpr (sizeof(TIn) == 1) {
+    if (bq)
+      return vec ? launch<TIn, C, W2, U, 1, true>(tm, p, smem, st)
+                 : launch<TIn, C, W2, U, 0, true>(tm, p, smem, st);
+  }
+  return vec ? launch<TIn, C, W2, U, 1, false>(tm, p, smem, st)
+             : launch<TIn, C, W2, U, 0, false>(tm, p, smem, st);
 }
 
 }  // namespace small
@@ -358,10 +442,11 @@ static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int
                    (W2 % 2 == 0 ? (ldo % 4 == 0 && (oa & 15u) == 0) : (ldo % 2 == 0 && (oa & 7u) == 0));
   *done = true;
   const bool avg = l.U != 0;
-  if (t.C == 4 && W2 == 1) return avg ? launch_v<TIn, 4, 1, 4>(tm, p, smem, vec, st) : launch_v<TIn, 4, 1, 0>(tm, p, smem, vec, st);
-  if (t.C == 4 && W2 == 2) return avg ? launch_v<TIn, 4, 2, 4>(tm, p, smem, vec, st) : launch_v<TIn, 4, 2, 0>(tm, p, smem, vec, st);
-  if (t.C == 8 && W2 == 1) return avg ? launch_v<TIn, 8, 1, 8>(tm, p, smem, vec, st) : launch_v<TIn, 8, 1, 0>(tm, p, smem, vec, st);
-  if (t.C == 8 && W2 == 2) return avg ? launch_v<TIn, 8, 2, 8>(tm, p, smem, vec, st) : launch_v<TIn, 8, 2, 0>(tm, p, smem, vec, st);
+  const bool bq = t.q_byte && knob_bq();
+  if (t.C == 4 && W2 == 1) return avg ? launch_v<TIn, 4, 1, 4>(tm, p, smem, vec, bq, st) : launch_v<TIn, 4, 1, 0>(tm, p, smem, vec, bq, st);
+  if (t.C == 4 && W2 == 2) return avg ? launch_v<TIn, 4, 2, 4>(tm, p, smem, vec, bq, st) : launch_v<TIn, 4, 2, 0>(tm, p, smem, vec, bq, st);
+  if (t.C == 8 && W2 == 1) return avg ? launch_v<TIn, 8, 1, 8>(tm, p, smem, vec, bq, st) : launch_v<TIn, 8, 1, 0>(tm, p, smem, vec, bq, st);
+  if (t.C == 8 && W2 == 2) return avg ? launch_v<TIn, 8, 2, 8>(tm, p, smem, vec, bq, st) : launch_v<TIn, 8, 2, 0>(tm, p, smem, vec, bq, st);
   *done = false;
   return cudaSuccess;
 }

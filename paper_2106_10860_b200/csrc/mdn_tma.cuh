@@ -81,6 +81,7 @@ struct DevInfo {
 DevInfo dev_info();
 bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int SW, int R, int es);
 int knob_hint();
+bool knob_bq();
 
 }  // namespace fast
 }  // namespace mdn
