@@ -66,11 +66,16 @@ struct SParams {
   float* out;
 };
 
-// Code-row stride in words: 16-B aligned and conflict-free for the lane-per-row
-// LDS.128 reads (C = 8: 48-B rows spread a quarter-warp over all 32 banks).
+// Code rows are C words (one table address per codebook). C = 8: rows whose
+// index has bit 2 set store their two 16-B halves swapped (word c ^ 4), so the
+// encoder's stores (4 rows x 8 codebooks) and the scanner's lane-per-row
+// LDS.128 reads (a quarter-warp = rows 8k..8k+7) both cover all 32 banks
+// once. The scanner then sees codebook c ^ 4 in slot c: harmless for the exact
+// sum, and for the App. D averaging tree over the 8 codebooks an XOR of the
+// leaf index only swaps the (commutative) operands of some mu(a, b).
 template <int C>
 struct CodeStride {
-  static constexpr int value = C == 8 ? 12 : 4;
+  static constexpr int value = C;
 };
 
 // Algorithm 1 with the tree in registers: p <- 2p + [x_t >= v^t_p] where the
@@ -293,7 +298,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         code[it] = lut_c + 4u * W2 * tree_code<float>(x[it][0], x[it][1], x[it][2], x[it][3], th);
     }
 #pragma unroll
-    for (int it = 0; it < C; ++it) s_code[(it * RPW + rs) * CS + c] = code[it];
+    for (int it = 0; it < C; ++it) {
+      const int rr = it * RPW + rs;
+      s_code[rr * CS + (C == 8 ? (c ^ (rr & 4)) : c)] = code[it];
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);           // this chunk's rows are consumed
     // ---- scan row `lane` ----
