@@ -14,7 +14,7 @@
 //                   output columns ("f"; the paper's column-pair
 //                   fusion, App. D, generalised to 4 columns per lookup);
 //                   exact sums in 2 x 16-bit SWAR lanes, or the App. D
-//                   averaging tree with __vavgu4 (L335, L697-706); then
+//                   averaging tree (4-lane byte average, L335, L697-706); then
 //                   out = alpha * S + beta (Eq. 1) and coalescing-friendly
 //                   128-bit stores.
 //
@@ -64,6 +64,7 @@ struct Params {
   int slab_e;                     // shared-memory elements (of the input type) per slab, 128-B aligned
   int pad_e;                      // row pitch = SW + pad_e elements (16 bytes of padding)
   int M;
+  bool pair;                      // M even, ldo even, out 8-B aligned: 8-byte stores
   int l2_hint;                    // 0 none (default), 1 evict_first, 2 evict_last, 3 evict_normal
   float alpha_eff, beta32;
   const uint32_t* lut;            // global [C][W][16]
@@ -83,8 +84,18 @@ struct Params {
 // Exact mode (U == 0): ae[w] / ao[w] hold the even / odd output columns of
 // word w in two 16-bit lanes (S <= 255 C < 2^16 for C <= 256).
 // Averaging mode: per block of U consecutive codebooks the halves-recursion
-// tree of rounded averages (mu(a,b) = (a+b+1)>>1 per byte, __vavgu4), and the
+// tree of rounded averages (mu(a,b) = (a+b+1)>>1 per byte, avg8), and the
 // block results are summed exactly (App. D, reading R16/R17).
+// mu(a, b) = floor((a + b + 1) / 2) on 4 byte lanes (App. D) as
+// (a | b) - (((a ^ b) & 0xFE..) >> 1): per byte a | b = (a & b) + (a ^ b) can
+// never borrow, and the mask keeps each byte's low bit from shifting into its
+// neighbour. 4 ALU ops (LOP3, LOP3, SHF, IADD) against 5 for __vavgu4.
+__device__ __forceinline__ uint32_t avg8(uint32_t a, uint32_t b) {
+  uint32_t x;   // (a ^ b) & 0xFEFEFEFE in one LOP3 (inline: LLVM would re-canonicalise it)
+  asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(x) : "r"(a), "r"(b), "r"(0xFEFEFEFEu));
+  return (a | b) - (x >> 1);
+}
+
 template <int C, int W, int U, class Words>
 __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Words words,
                                           uint32_t (&ae)[W], uint32_t (&ao)[W]) {
@@ -134,7 +145,7 @@ __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Word
 #pragma unroll
         for (int s = 1; s < U; s *= 2)
 #pragma unroll
-          for (int i = 0; i < U; i += 2 * s) v[i] = __vavgu4(v[i], v[i + s]);
+          for (int i = 0; i < U; i += 2 * s) v[i] = avg8(v[i], v[i + s]);
         ae[w] += v[0] & 0x00FF00FFu;
         ao[w] += __byte_perm(v[0], 0u, 0x4341);
       }
@@ -144,9 +155,11 @@ __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Word
 
 // out[m] = fl32(alpha_eff * S'[m] + beta32): S' < 2^16 is exact in fp32 and
 // alpha_eff a power of two, so the FMA's single rounding equals the oracle's.
+// pair: (non-VEC) M even and the row 8-byte aligned -> 8-byte stores.
 template <int W, bool VEC>
 __device__ __forceinline__ void store_row(float* __restrict__ o, int M, const uint32_t (&ae)[W],
-                                          const uint32_t (&ao)[W], float a, float b) {
+                                          const uint32_t (&ao)[W], float a, float b,
+                                          bool pair = false) {
 #pragma unroll
   for (int w = 0; w < W; ++w) {
     float4 f;
@@ -156,6 +169,10 @@ __device__ __forceinline__ void store_row(float* __restrict__ o, int M, const ui
     f.w = __fmaf_rn(a, (float)(ao[w] >> 16), b);
     if constexpr (VEC) {
       *reinterpret_cast<float4*>(o + 4 * w) = f;
+    } else if (pair) {
+      const int m = 4 * w;
+      if (m + 1 < M) *reinterpret_cast<float2*>(o + m) = make_float2(f.x, f.y);
+      if (m + 3 < M) *reinterpret_cast<float2*>(o + m + 2) = make_float2(f.z, f.w);
     } else {
       const int m = 4 * w;
       if (m + 0 < M) o[m + 0] = f.x;
@@ -415,7 +432,8 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
         uint32_t ae[W], ao[W];
         scan_core<C, W, U>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
         if (k == KR - 1) mbar_arrive(&cempty[b]);
-        if (row < p.N) store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32);
+        if (row < p.N)
+          store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32, p.pair);
       }
     }
   }
@@ -710,6 +728,7 @@ static cudaError_t amm_fast(const TreesDev& t, const LutsDev& l, const TIn* A, i
   const int sf = subf_for(t, g, es);
   p.ldo = ldo;
   p.M = l.M;
+  p.pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
   p.alpha_eff = l.alpha_eff;
   p.beta32 = l.beta32;
   p.lut = l.words;
