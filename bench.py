@@ -135,6 +135,17 @@ def _bench_rows(name, rank, ws, device):
     return torch.from_numpy(A).to(device).repeat(reps, 1)
 
 
+def split_dims(model_blob: bytes):
+    """Distinct split columns of a model.mdnm v1 blob (format: include/maddness.h)."""
+    import struct
+    C, D = struct.unpack_from("<II", model_blob, 8)
+    off, dims = 48, set()
+    for _ in range(C):
+        dims.update(struct.unpack_from("<4H", model_blob, off + 8))
+        off += 8 + 8 + 60
+    return sorted(dims)
+
+
 def _config_B(name):
     from datagen.synth import CONFIGS, relu_B, sobel_B
     return relu_B(name) if CONFIGS[name].kind == "relu" else sobel_B(CONFIGS[name].D)
@@ -278,6 +289,15 @@ def run(args):
     u8 = A.dtype == torch.uint8
     amm_fn = mdn.mdn_amm_u8 if u8 else mdn.mdn_amm
     enc_fn = mdn.mdn_encode_u8 if u8 else mdn.mdn_encode
+    col = args.layout == "col"
+    if col:
+        # Column-major A: the same rows stored as At = A^T (D x N).
+        assert not u8 and op != "scan", "--layout col: fp32 A, amm or encode"
+        A_rows = A[:1 << 16].clone() if rank == 0 else None    # for NMSE / cuBLAS context
+        A = A.t().contiguous()
+        torch.cuda.synchronize()
+        amm_fn = lambda m, l, At, o, stream=None: mdn.mdn_amm_cm(m, l, At, o, stream=stream)
+        enc_fn = lambda m, At, c, stream=None: mdn.mdn_encode_cm(m, At, c, stream=stream)
 
     def step():
         if op == "amm":
@@ -311,13 +331,15 @@ def run(args):
     rows_total = n * ws * args.steps
     value = rows_total / (elapsed_ms / 1e3)
     ea = A.element_size()            # 4 (fp32 A) or 1 (8-bit A)
-    bytes_per_row = {"amm": ea * spec.D + 4 * spec.M, "encode": ea * spec.D + (spec.C + 1) // 2,
+    # Column-major A: only the distinct split columns S are read (4 |S| bytes/row).
+    a_bytes = 4 * len(split_dims(model_blob)) if col else ea * spec.D
+    bytes_per_row = {"amm": a_bytes + 4 * spec.M, "encode": a_bytes + (spec.C + 1) // 2,
                      "scan": (spec.C + 1) // 2 + 4 * spec.M}[op]
 
     # Achievable-bandwidth probe: a plain streaming kernel with the same byte
     # mix (read A, write M floats per row), timed the same way.
     probe = None
-    if op == "amm" and not u8 and spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
+    if op == "amm" and not u8 and not col and spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
         probe_out = torch.empty_like(out)     # never overwrite the step's output
         for _ in range(2):
             mdn.mdn_stream_probe(A, probe_out, stream=stream)
@@ -343,11 +365,12 @@ def run(args):
         B = _config_B(name)
         Bd = torch.from_numpy(B).cuda()
         rows = 65536
-        exact = (A[:rows].double() @ Bd.double())
+        Ar = A_rows if col else A[:rows]
+        exact = (Ar.double() @ Bd.double())
         nmse = float(((out[:rows].double() - exact) ** 2).sum() / (exact ** 2).sum())
         torch.backends.cuda.matmul.allow_tf32 = False
         ref = torch.empty_like(out)
-        Af = A.float() if u8 else A
+        Af = A.float() if u8 else (A.t() if col else A)
         torch.matmul(Af, Bd, out=ref)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -361,7 +384,7 @@ def run(args):
 
     # --- e2e: the same metric through the public API with HOST buffers --------
     e2e = None
-    if op == "amm" and not u8 and (rank == 0 or ws > 1):
+    if op == "amm" and not u8 and not col and (rank == 0 or ws > 1):
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
                                  n_slots=3)
         n_e2e = min(n, (1 << 32) // (4 * spec.D))     # <= 4 GiB of pinned host A per rank
@@ -386,7 +409,7 @@ def run(args):
 
     # --- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only ---
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and op == "amm":
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and op == "amm" and not col:
         import oracle as O
         om = O.read_model(model_blob)
         oluts = O.make_luts(om, B, args.mode, spec.U)
@@ -412,7 +435,8 @@ def run(args):
             except Exception:
                 traffic = None
         line = {
-            "metric": _metric(name) + ("" if op == "amm" else f" [{op} only]"), "value": value,
+            "metric": _metric(name) + ("" if op == "amm" else f" [{op} only]")
+                      + (" [column-major A]" if col else ""), "value": value,
             "unit": "rows/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
@@ -420,7 +444,8 @@ def run(args):
             "config": {"workload": f"{name}: D={spec.D}, M={spec.M}, C={spec.C}, K=16, {args.mode} sum"
                        + (f" (U={spec.U})" if args.mode == "avg" else "")
                        + ("; relu low-rank rows" if spec.kind == "relu" else "; 3x3x3 image patches")
-                       + ", oracle-trained trees / ridge prototypes",
+                       + ", oracle-trained trees / ridge prototypes"
+                       + ("; A stored column-major (At = A^T), only the split columns read" if col else ""),
                        "rows_per_gpu": n, "global_rows_per_step": n * ws,
                        "A_bytes_per_gpu": n * 4 * spec.D,
                        "l2": f"inputs {n * 4 * spec.D / 2**30:.1f} GiB per GPU > 126 MB L2; no flush",
@@ -430,7 +455,8 @@ def run(args):
                          "frac": achieved_gbs / peak, "peak_kind": peak_kind,
                          "traffic": traffic,
                          "algorithmic_bytes_per_launch": n * bytes_per_row,
-                         "kernel": mdn.mdn_amm_variant(model, luts, spec.D) if op == "amm" else op,
+                         "kernel": ("k_amm_cm" if col else mdn.mdn_amm_variant(model, luts, spec.D))
+                                   if op == "amm" else op,
                          "frac_of_stream_probe": (achieved_gbs / probe["gbs"]) if probe else None},
             "stream_probe": probe,
             "cpu_baseline": cpu,
@@ -461,6 +487,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--op", choices=["amm", "encode", "scan"], default="amm",
                     help="amm (the hot path, default) or the unfused halves, for DESIGN.md")
+    ap.add_argument("--layout", choices=["row", "col"], default="row",
+                    help="row-major A (default) or column-major A (SURVEY N2: split-column gather)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -151,6 +151,24 @@ int mdn_encode_u8(const mdn_model* model, const uint8_t* A, int64_t N, int64_t l
 int mdn_amm_u8(const mdn_model* model, const mdn_luts* luts, const uint8_t* A, int64_t N,
                int64_t lda, float* out, int64_t ldo, void* stream);
 
+/* ------------------------------------------- column-major A -- */
+
+/* g and the fused path for COLUMN-MAJOR A: "[Algorithm 1] only depends on a
+ * constant number of indices in the input vector, and can easily be
+ * vectorized provided that the matrix whose rows are being encoded is stored
+ * in column-major order"; its cost per row is O(C), not O(D)
+ * (L431). Only the <= 4C split columns of A are read.
+ *   At     device fp32, D x N row-major (= A column-major): element (n, j) of
+ *          A is At[j * ldt + n]; ldt >= N (elements).
+ *   codes  as mdn_encode (row-major N x ceil(C/2)); out as mdn_amm (row-major
+ *          N x M, ldo >= M). Results are bit-identical to mdn_encode /
+ *          mdn_amm on the same A stored row-major.
+ * Errors as mdn_encode / mdn_amm (ldt < N: MDN_EINVAL). */
+int mdn_encode_cm(const mdn_model* model, const float* At, int64_t N, int64_t ldt,
+                  uint8_t* codes, void* stream);
+int mdn_amm_cm(const mdn_model* model, const mdn_luts* luts, const float* At, int64_t N,
+               int64_t ldt, float* out, int64_t ldo, void* stream);
+
 /* ----------------------------------------------------- end-to-end (host) -- */
 
 /* A pipelined executor for HOST buffers: row chunks are copied host->device,

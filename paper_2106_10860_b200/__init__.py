@@ -55,6 +55,8 @@ _SIGS = {
     "mdn_stream_probe": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
     "mdn_encode_u8": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "mdn_amm_u8": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "mdn_encode_cm": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
+    "mdn_amm_cm": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -241,6 +243,37 @@ def mdn_amm_u8(model: Model, luts: Luts, A, out, stream=None):
         raise ValueError("out must be N x M")
     _check(_lib.mdn_amm_u8(model._h, luts._h, pa, A.shape[0], A.stride(0), po, out.stride(0),
                            _stream_ptr(stream)), "mdn_amm_u8")
+    return out
+
+
+def _colmajor(At, what):
+    """At: D x N CUDA float32 tensor with unit column stride (A column-major)."""
+    pa = _dev_ptr(At, "float32", what)
+    return pa, At.shape[1], At.stride(0)
+
+
+def mdn_encode_cm(model: Model, At, codes, stream=None):
+    """g for column-major A: At = A^T, D x N."""
+    pa, N, ldt = _colmajor(At, "At")
+    pc = _dev_ptr(codes, "uint8", "codes")
+    if At.shape[0] != model.D:
+        raise ValueError("At must be D x N")
+    if codes.shape != (N, (model.C + 1) // 2) or not codes.is_contiguous():
+        raise ValueError("codes must be contiguous N x ceil(C/2)")
+    _check(_lib.mdn_encode_cm(model._h, pa, N, ldt, pc, _stream_ptr(stream)), "mdn_encode_cm")
+    return codes
+
+
+def mdn_amm_cm(model: Model, luts: Luts, At, out, stream=None):
+    """Fused g + f + dequant for column-major A (At = A^T, D x N); out is N x M."""
+    pa, N, ldt = _colmajor(At, "At")
+    po = _dev_ptr(out, "float32", "out")
+    if At.shape[0] != model.D:
+        raise ValueError("At must be D x N")
+    if out.shape != (N, luts.M):
+        raise ValueError("out must be N x M")
+    _check(_lib.mdn_amm_cm(model._h, luts._h, pa, N, ldt, po, out.stride(0), _stream_ptr(stream)),
+           "mdn_amm_cm")
     return out
 
 

@@ -1,0 +1,270 @@
+// Column-major A: the split-column gather encoder.
+//
+// Algorithm 1 "only depends on a constant number of indices in the input
+// vector, and can easily be vectorized provided that the matrix whose rows are
+// being encoded is stored in column-major order", and its cost
+// per row is O(C) rather than O(D) (L431). With A stored column-major (At =
+// A^T, D x N, row stride ldt >= N) the kernel reads ONLY the <= 4C split
+// columns, each as fully coalesced 128-byte warp loads (lane = row), so the
+// HBM bytes per row are 4 |S| + 4M (|S| = distinct split dims) instead of
+// 4D + 4M: 912 vs 2448 for the CIFAR-100-shaped config.
+//
+// The fused path for heavy scans (W >= 8 table words per code) runs the
+// warp-specialised TMA kernel of mdn_fast.cu with a [slot][row] stage layout
+// (launch_amm_ws_cm); everything else runs here.
+//
+// k_amm_cm: thread per row. For each group of 8 codebooks the 32 split values
+// are loaded (streaming, evict-first: each is used once), Algorithm 1 runs on
+// thresholds resident in shared memory, and the packed codes feed the same
+// shared-memory table scan as the row-major fused kernel (mdn_scan.cuh); the
+// codes never leave registers. ENC_ONLY writes the packed codes instead.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "mdn_internal.h"
+#include "mdn_scan.cuh"
+#include "mdn_tma.cuh"
+
+namespace mdn {
+namespace fast {
+namespace colmajor {
+
+constexpr int THREADS = 256;
+
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float v;
+  asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+// Algorithm 1 (L228-248) for G codebooks of one row; x[i][t] = the row's value
+// in split column dims[c0 + i][t]. 0-based: p <- 2p + [x_t >= v^t_p].
+template <int G>
+__device__ __forceinline__ uint32_t encode_group(const float (&x)[G][4], const float* __restrict__ s_thr,
+                                                 int c0) {
+  uint32_t word = 0;
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    const float* th = s_thr + 16 * (c0 + i);
+    uint32_t p = x[i][0] >= th[0] ? 1u : 0u;
+    p = 2u * p + (x[i][1] >= th[1 + p] ? 1u : 0u);
+    p = 2u * p + (x[i][2] >= th[3 + p] ? 1u : 0u);
+    p = 2u * p + (x[i][3] >= th[7 + p] ? 1u : 0u);
+    word |= p << (4 * i);
+  }
+  return word;
+}
+
+struct CmParams {
+  const float* At;
+  int64_t N, ldt, ldo;
+  const uint16_t* dims;   // [C][4]
+  const float* thr;       // [C][16]
+  const uint32_t* lut;    // [C][W][16]
+  float* out;
+  uint8_t* codes;
+  int M;
+  bool pair;
+  float alpha_eff, beta32;
+};
+
+template <int C, int W, int U, bool VEC, bool ENC_ONLY>
+__global__ void __launch_bounds__(THREADS) k_amm_cm(const CmParams p) {
+  constexpr int G = C >= 8 ? 8 : C;
+  constexpr int NG = C / G;
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* s_thr = reinterpret_cast<float*>(smem);                       // [C][16]
+  int64_t* s_col = reinterpret_cast<int64_t*>(s_thr + 16 * C);         // [C][4] element offsets
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_col + 4 * C);        // [C][W][16]
+  for (int i = threadIdx.x; i < 16 * C; i += blockDim.x) s_thr[i] = p.thr[i];
+  for (int i = threadIdx.x; i < 4 * C; i += blockDim.x) s_col[i] = (int64_t)p.dims[i] * p.ldt;
+  if constexpr (!ENC_ONLY) {
+    const uint4* src = reinterpret_cast<const uint4*>(p.lut);
+    uint4* dst = reinterpret_cast<uint4*>(s_lut);
+    for (int i = threadIdx.x; i < C * W * 4; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < p.N;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const float* a = p.At + row;
+    uint32_t cw[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      float x[G][4];
+#pragma unroll
+      for (int i = 0; i < G; ++i)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) x[i][t] = ld_stream(a + s_col[(g * G + i) * 4 + t]);
+      cw[g] = encode_group<G>(x, s_thr, g * G);
+    }
+    if constexpr (ENC_ONLY) {
+      if constexpr (C >= 8) {
+#pragma unroll
+        for (int g = 0; g < NG; ++g) reinterpret_cast<uint32_t*>(p.codes + row * (C / 2))[g] = cw[g];
+      } else if constexpr (C == 4) {
+        reinterpret_cast<uint16_t*>(p.codes + row * 2)[0] = (uint16_t)cw[0];
+      } else {
+        p.codes[row] = (uint8_t)cw[0];
+      }
+    } else {
+      uint32_t ae[W], ao[W];
+      scan_core<C, W, U, true>(s_lut, [&](int g) { return cw[g]; }, ae, ao);
+      store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32, p.pair);
+    }
+  }
+}
+
+// Generic fallback: any C (<= MAX_C), any M / U, any alignment.
+__global__ void k_amm_cm_generic(TreesDev t, LutsDev l, const float* __restrict__ At, int64_t N,
+                                 int64_t ldt, float* __restrict__ out, int64_t ldo,
+                                 uint8_t* __restrict__ codes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* s_thr = reinterpret_cast<float*>(smem);
+  int* s_dims = reinterpret_cast<int*>(s_thr + t.C * THR_STRIDE);
+  for (int i = threadIdx.x; i < t.C * THR_STRIDE; i += blockDim.x) s_thr[i] = t.thr[i];
+  for (int i = threadIdx.x; i < t.C * 4; i += blockDim.x) s_dims[i] = t.dims[i];
+  __syncthreads();
+  uint8_t code_row[MAX_C / 2];
+  const int nb = (t.C + 1) / 2;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < N;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    for (int i = 0; i < nb; ++i) code_row[i] = 0;
+    for (int c = 0; c < t.C; ++c) {
+      int q = 0;
+      for (int lv = 0; lv < 4; ++lv) {
+        const float x = At[(int64_t)s_dims[c * 4 + lv] * ldt + row];
+        q = 2 * q + (x >= s_thr[c * THR_STRIDE + (1 << lv) - 1 + q] ? 1 : 0);
+      }
+      code_row[c >> 1] |= (uint8_t)(q << (4 * (c & 1)));
+    }
+    if (codes) {
+      for (int i = 0; i < nb; ++i) codes[row * nb + i] = code_row[i];
+      continue;
+    }
+    for (int m = 0; m < l.M; ++m) {
+      int s = 0;
+      if (l.U == 0) {
+        for (int c = 0; c < l.C; ++c)
+          s += l.tq[((int64_t)c * K + ((code_row[c >> 1] >> (4 * (c & 1))) & 15)) * l.M + m];
+      } else {
+        // App. D halves recursion, evaluated as a binary counter (as mdn_generic.cu)
+        for (int b = 0; b < l.C / l.U; ++b) {
+          int stack[8], top = 0;
+          for (int i = 0; i < l.U; ++i) {
+            const int c = b * l.U + i;
+            int v = l.tq[((int64_t)c * K + ((code_row[c >> 1] >> (4 * (c & 1))) & 15)) * l.M + m];
+            int lvl = 0;
+            for (int ii = i; ii & 1; ii >>= 1) v = (stack[lvl++] + v + 1) >> 1;
+            stack[lvl] = v;
+            top = lvl;
+          }
+          s += stack[top];
+        }
+      }
+      out[row * ldo + m] = __fmaf_rn(l.alpha_eff, (float)s, l.beta32);
+    }
+  }
+}
+
+template <int C, int W, int U, bool VEC, bool ENC>
+cudaError_t launch(const CmParams& p, cudaStream_t s) {
+  auto k = k_amm_cm<C, W, U, VEC, ENC>;
+  const size_t smem = 16 * C * 4 + 4 * C * 8 + (ENC ? 0 : (size_t)C * W * 16 * 4);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t blocks = (p.N + THREADS - 1) / THREADS;
+  const int64_t cap = (int64_t)dev_info().sms * per_sm;
+  if (blocks > cap) blocks = cap;
+  k<<<(unsigned)blocks, THREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+#define MDN_CM_COMBOS(X) \
+  X(4, 1, 0) X(4, 1, 4) X(8, 1, 0) X(8, 1, 8) X(8, 2, 0) X(8, 2, 8)                    \
+  X(16, 1, 0) X(16, 1, 16) X(16, 3, 0) X(16, 3, 16) X(16, 4, 0) X(16, 4, 16)            \
+  X(32, 1, 0) X(32, 1, 16) X(32, 3, 0) X(32, 3, 16) X(32, 4, 0) X(32, 4, 16)            \
+  X(32, 25, 0) X(32, 25, 16) X(64, 3, 0) X(64, 3, 16) X(64, 4, 0) X(64, 4, 16)
+
+}  // namespace colmajor
+}  // namespace fast
+
+using namespace fast::colmajor;
+
+static cudaError_t cm_generic(const TreesDev& t, const LutsDev* l, const float* At, int64_t N,
+                              int64_t ldt, float* out, int64_t ldo, uint8_t* codes, cudaStream_t s) {
+  const size_t smem = (size_t)t.C * THR_STRIDE * 4 + (size_t)t.C * 4 * 4;
+  int64_t blocks = (N + 255) / 256;
+  const int64_t cap = (int64_t)fast::dev_info().sms * 8;
+  if (blocks > cap) blocks = cap;
+  LutsDev ld{};
+  if (l) ld = *l;
+  k_amm_cm_generic<<<(unsigned)blocks, 256, smem, s>>>(t, ld, At, N, ldt, out, ldo, codes);
+  return cudaGetLastError();
+}
+
+// MDN_CM_SIMPLE=1 forces the thread-per-row kernel below (A/B comparisons only).
+static bool cm_simple() {
+  static int v = [] { const char* e = getenv("MDN_CM_SIMPLE"); return e ? atoi(e) : 0; }();
+  return v != 0;
+}
+
+cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
+                          int64_t ldt, float* out, int64_t ldo, cudaStream_t s) {
+  if (!cm_simple()) {
+    bool done = false;
+    cudaError_t e = launch_amm_ws_cm(t, l, At, N, ldt, out, ldo, s, &done);
+    if (done) return e;
+  }
+  CmParams p{};
+  p.At = At;
+  p.N = N;
+  p.ldt = ldt;
+  p.ldo = ldo;
+  p.dims = t.dims;
+  p.thr = t.thr;
+  p.lut = l.words;
+  p.out = out;
+  p.M = l.M;
+  p.pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
+  p.alpha_eff = l.alpha_eff;
+  p.beta32 = l.beta32;
+  const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+#define X(c, w, u)                                                                   \
+  if (t.C == c && l.W == w && l.U == u)                                              \
+    return vec ? launch<c, w, u, true, false>(p, s) : launch<c, w, u, false, false>(p, s);
+  MDN_CM_COMBOS(X)
+#undef X
+  return cm_generic(t, &l, At, N, ldt, out, ldo, nullptr, s);
+}
+
+cudaError_t launch_encode_cm(const TreesDev& t, const float* At, int64_t N, int64_t ldt,
+                             uint8_t* codes, cudaStream_t s) {
+  // Encode only: the thread-per-row kernel (measured 0.86-0.88 of HBM on
+  // 4 |S| + C/2 bytes per row; the TMA column-box variant reached 0.38).
+  CmParams p{};
+  p.At = At;
+  p.N = N;
+  p.ldt = ldt;
+  p.dims = t.dims;
+  p.thr = t.thr;
+  p.codes = codes;
+  const uintptr_t ca = reinterpret_cast<uintptr_t>(codes);
+  const bool aligned = t.C >= 8 ? (ca & 3u) == 0 : (t.C == 4 ? (ca & 1u) == 0 : true);
+  if (aligned) {
+    switch (t.C) {
+      case 4: return launch<4, 1, 0, false, true>(p, s);
+      case 8: return launch<8, 1, 0, false, true>(p, s);
+      case 16: return launch<16, 1, 0, false, true>(p, s);
+      case 32: return launch<32, 1, 0, false, true>(p, s);
+      case 64: return launch<64, 1, 0, false, true>(p, s);
+    }
+  }
+  return cm_generic(t, nullptr, At, N, ldt, nullptr, 0, codes, s);
+}
+
+}  // namespace mdn

@@ -34,6 +34,7 @@
 
 #include "mdn_internal.h"
 #include "mdn_tma.cuh"
+#include "mdn_scan.cuh"
 
 namespace mdn {
 namespace fast {
@@ -42,6 +43,7 @@ constexpr int BR = 256;                  // rows per tile
 constexpr int NB = 3;                    // code ring depth (tiles)
 constexpr int NS_MAX = 8;                // A stage ring depth cap
 constexpr int BAR_BYTES = 256;
+constexpr int CM = -1;                   // SUBF value of the column-major-A variant
 
 // Warp roles. Per row an encoder spends ~25 instructions per codebook
 // (4 split-dim loads, 4 threshold gathers, compares), a scanner ~4W per
@@ -72,130 +74,11 @@ struct Params {
   const uint16_t* sub;            // global [C] subspace begin
   const float* thr;               // global [C][16]
   const uint16_t* q;              // global [C][16] 8-bit split values ceil(v) (uint8 input)
+  const uint16_t* slot;           // column-major A: global [D] stage slot of each split column
+  const uint16_t* cols;           // column-major A: global [nslab] split column of each slot
   float* out;
   uint8_t* codes;                 // encode-only output
 };
-
-// ------------------------------------------------------------ scan core --
-
-// Accumulate the W table words of every codebook for one row.
-//   words(g): the g-th 32-bit word of the row's packed codes (8 codes, low
-//   nibble first; for C < 8 only the low 4C bits are used).
-// Exact mode (U == 0): ae[w] / ao[w] hold the even / odd output columns of
-// word w in two 16-bit lanes (S <= 255 C < 2^16 for C <= 256).
-// Averaging mode: per block of U consecutive codebooks the halves-recursion
-// tree of rounded averages (mu(a,b) = (a+b+1)>>1 per byte, avg8), and the
-// block results are summed exactly (App. D, reading R16/R17).
-// mu(a, b) = floor((a + b + 1) / 2) on 4 byte lanes (App. D) as
-// (a | b) - (((a ^ b) & 0xFE..) >> 1): per byte a | b = (a & b) + (a ^ b) can
-// never borrow, and the mask keeps each byte's low bit from shifting into its
-// neighbour. 4 ALU ops (LOP3, LOP3, SHF, IADD) against 5 for __vavgu4.
-__device__ __forceinline__ uint32_t avg8(uint32_t a, uint32_t b) {
-  uint32_t x;   // (a ^ b) & 0xFEFEFEFE in one LOP3 (inline: LLVM would re-canonicalise it)
-  asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(x) : "r"(a), "r"(b), "r"(0xFEFEFEFEu));
-  return (a | b) - (x >> 1);
-}
-
-template <int C, int W, int U, class Words>
-__device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Words words,
-                                          uint32_t (&ae)[W], uint32_t (&ao)[W]) {
-#pragma unroll
-  for (int w = 0; w < W; ++w) ae[w] = ao[w] = 0u;
-  if constexpr (U == 0) {
-    constexpr int G = C >= 8 ? 8 : C;
-#pragma unroll 1
-    for (int g = 0; g < C / G; ++g) {
-      const uint32_t cw = words(g);
-      const uint32_t* lg = lut + g * G * W * 16;
-#pragma unroll
-      for (int i = 0; i < G; i += 2) {
-        const uint32_t* p0 = lg + (i * W) * 16 + ((cw >> (4 * i)) & 15u);
-        const uint32_t* p1 = lg + ((i + 1) * W) * 16 + ((cw >> (4 * i + 4)) & 15u);
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const uint32_t a = p0[w * 16], b = p1[w * 16];
-          ae[w] += (a & 0x00FF00FFu) + (b & 0x00FF00FFu);
-          ao[w] += __byte_perm(a, 0u, 0x4341) + __byte_perm(b, 0u, 0x4341);
-        }
-      }
-    }
-  } else {
-    static_assert((U & (U - 1)) == 0 && C % U == 0, "U must be a power of two dividing C");
-#pragma unroll 1
-    for (int blk = 0; blk < C / U; ++blk) {
-      const uint32_t* p[U];
-#pragma unroll
-      for (int i = 0; i < U; ++i) {
-        const int c = blk * U + i;  // runtime blk, static i
-        uint32_t cw;
-        if constexpr (U >= 8) {
-          cw = words(blk * (U / 8) + i / 8);
-          p[i] = lut + (c * W) * 16 + ((cw >> (4 * (i % 8))) & 15u);
-        } else {
-          const int cc = blk * U + i;
-          cw = words(cc >> 3);
-          p[i] = lut + (c * W) * 16 + ((cw >> (4 * (cc & 7))) & 15u);
-        }
-      }
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        uint32_t v[U];
-#pragma unroll
-        for (int i = 0; i < U; ++i) v[i] = p[i][w * 16];
-#pragma unroll
-        for (int s = 1; s < U; s *= 2)
-#pragma unroll
-          for (int i = 0; i < U; i += 2 * s) v[i] = avg8(v[i], v[i + s]);
-        ae[w] += v[0] & 0x00FF00FFu;
-        ao[w] += __byte_perm(v[0], 0u, 0x4341);
-      }
-    }
-  }
-}
-
-// out[m] = fl32(alpha_eff * S'[m] + beta32): S' < 2^16 is exact in fp32 and
-// alpha_eff a power of two, so the FMA's single rounding equals the oracle's.
-// pair: (non-VEC) M even and the row 8-byte aligned -> 8-byte stores.
-template <int W, bool VEC>
-__device__ __forceinline__ void store_row(float* __restrict__ o, int M, const uint32_t (&ae)[W],
-                                          const uint32_t (&ao)[W], float a, float b,
-                                          bool pair = false) {
-#pragma unroll
-  for (int w = 0; w < W; ++w) {
-    float4 f;
-    f.x = __fmaf_rn(a, (float)(ae[w] & 0xFFFFu), b);
-    f.y = __fmaf_rn(a, (float)(ao[w] & 0xFFFFu), b);
-    f.z = __fmaf_rn(a, (float)(ae[w] >> 16), b);
-    f.w = __fmaf_rn(a, (float)(ao[w] >> 16), b);
-    if constexpr (VEC) {
-      *reinterpret_cast<float4*>(o + 4 * w) = f;
-    } else if (pair) {
-      const int m = 4 * w;
-      if (m + 1 < M) *reinterpret_cast<float2*>(o + m) = make_float2(f.x, f.y);
-      if (m + 3 < M) *reinterpret_cast<float2*>(o + m + 2) = make_float2(f.z, f.w);
-    } else {
-      const int m = 4 * w;
-      if (m + 0 < M) o[m + 0] = f.x;
-      if (m + 1 < M) o[m + 1] = f.y;
-      if (m + 2 < M) o[m + 2] = f.z;
-      if (m + 3 < M) o[m + 3] = f.w;
-    }
-  }
-}
-
-template <int W>
-__device__ __forceinline__ void store_sums(int32_t* __restrict__ o, int M, int scale,
-                                           const uint32_t (&ae)[W], const uint32_t (&ao)[W]) {
-#pragma unroll
-  for (int w = 0; w < W; ++w) {
-    const int m = 4 * w;
-    const int v[4] = {(int)(ae[w] & 0xFFFFu), (int)(ao[w] & 0xFFFFu), (int)(ae[w] >> 16),
-                      (int)(ao[w] >> 16)};
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (m + i < M) o[m + i] = v[i] * scale;
-  }
-}
 
 // ------------------------------------------------------------ fused kernel --
 
@@ -230,7 +113,7 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
   uint32_t word = 0;
   if constexpr (sizeof(TIn) == 1) {
     const int* s_q = reinterpret_cast<const int*>(s_thr);
-    uint32_t wv[SUBF == 0 ? 1 : G * SUBF];
+    uint32_t wv[SUBF <= 0 ? 1 : G * SUBF];
     if constexpr (SUBF > 0) {
       const uint4* src = reinterpret_cast<const uint4*>(rowp + s_base[c0]);
 #pragma unroll
@@ -244,7 +127,7 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
       const int c = c0 + i;
       const int4 o = *reinterpret_cast<const int4*>(s_off + 4 * c);
       int x0, x1, x2, x3;
-      if constexpr (SUBF == 0) {
+      if constexpr (SUBF <= 0) {
         x0 = rowp[o.x], x1 = rowp[o.y], x2 = rowp[o.z], x3 = rowp[o.w];
       } else if constexpr (SUBF == 1) {
         x0 = byte_of(wv[i], 0u, o.x), x1 = byte_of(wv[i], 0u, o.y);
@@ -267,7 +150,7 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
     const int c = c0 + i;
     const int4 o = *reinterpret_cast<const int4*>(s_off + 4 * c);
     float x0, x1, x2, x3;
-    if constexpr (SUBF == 0) {
+    if constexpr (SUBF <= 0) {
       x0 = rowp[o.x], x1 = rowp[o.y], x2 = rowp[o.z], x3 = rowp[o.w];
     } else {
       const float4* vb = reinterpret_cast<const float4*>(rowp + s_base[c]);
@@ -313,12 +196,14 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
   constexpr int OFF_THR = BAR_BYTES;
   constexpr int OFF_OFF = OFF_THR + 16 * C * 4;
   constexpr int OFF_BASE = OFF_OFF + 4 * C * 4;
-  constexpr int OFF_LUT = (OFF_BASE + C * 4 + 15) & ~15;
+  constexpr int OFF_COLS = OFF_BASE + C * 4;
+  constexpr int OFF_LUT = (OFF_COLS + (SUBF == CM ? 4 * C * 4 : 0) + 15) & ~15;
   constexpr int OFF_CODES = OFF_LUT + (ENC_ONLY ? 0 : C * W * 16 * 4);
   constexpr int OFF_STAGE = (OFF_CODES + (ENC_ONLY ? 0 : NB * BR * CBW * 4) + 127) & ~127;
   float* s_thr = reinterpret_cast<float*>(smem + OFF_THR);
   int* s_off = reinterpret_cast<int*>(smem + OFF_OFF);
   int* s_base = reinterpret_cast<int*>(smem + OFF_BASE);
+  int* s_cols = reinterpret_cast<int*>(smem + OFF_COLS);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
   uint32_t* s_codes = reinterpret_cast<uint32_t*>(smem + OFF_CODES);
   TIn* s_stage = reinterpret_cast<TIn*>(smem + OFF_STAGE);
@@ -335,8 +220,13 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
   }
   for (int i = tid; i < 4 * C; i += blockDim.x) {
     const int d = p.dims[i];
-    s_off[i] = SUBF ? d - p.sub[i / 4] : (d / p.SW) * p.slab_e + (d % p.SW);
+    if constexpr (SUBF == CM)
+      s_off[i] = p.slot[d] * p.slab_e;               // slot-major stage: [slot][row]
+    else
+      s_off[i] = SUBF ? d - p.sub[i / 4] : (d / p.SW) * p.slab_e + (d % p.SW);
   }
+  if constexpr (SUBF == CM)
+    for (int k = tid; k < p.nslab; k += blockDim.x) s_cols[k] = p.cols[k];
   for (int c = tid; c < C; c += blockDim.x) {
     const int b = p.sub[c];
     s_base[c] = (b / p.SW) * p.slab_e + (b % p.SW);
@@ -364,7 +254,11 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
   const int stages_per_tile = BR / p.R;
   if (warp == 0) {
     // ---------------- TMA producer ----------------
-    if (lane == 0) {
+    // Row-major A: lane 0 issues the nslab slab boxes of a stage. Column-major
+    // A: |S| single-column boxes per stage, issued by all 32 lanes (one lane
+    // issuing them serially caps the stage rate at ~140 cycles per box).
+    constexpr bool ALL_LANES = SUBF == CM;
+    if (ALL_LANES || lane == 0) {
       const uint32_t bytes = (uint32_t)(p.nslab * p.R * pitch * sizeof(TIn));
       const uint64_t pol = l2_policy(p.l2_hint);
       uint32_t q = 0;
@@ -374,13 +268,20 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
           mbar_wait(&empty[s], ((q / p.NS) & 1u) ^ 1u);
           const int64_t y = tile * BR + (int64_t)st * p.R;
           if (y >= p.N) {            // stage entirely past the last row: nothing to fetch
-            mbar_arrive(&full[s]);
+            if (lane == 0) mbar_arrive(&full[s]);
             continue;
           }
-          mbar_arrive_tx(&full[s], bytes);
+          if (lane == 0) mbar_arrive_tx(&full[s], bytes);
           TIn* dst = s_stage + (size_t)s * stage_e;
-          for (int k = 0; k < p.nslab; ++k)
-            tma_load_2d(dst + k * p.slab_e, &tmap, k * p.SW, (int)y, &full[s], p.l2_hint, pol);
+          if constexpr (SUBF == CM) {
+            // column-major A: one {R rows x 1 column} box per split column
+            __syncwarp();            // expect_tx before any complete_tx of this phase
+            for (int k = lane; k < p.nslab; k += 32)
+              tma_load_2d(dst + k * p.slab_e, &tmap, (int)y, s_cols[k], &full[s], p.l2_hint, pol);
+          } else {
+            for (int k = 0; k < p.nslab; ++k)
+              tma_load_2d(dst + k * p.slab_e, &tmap, k * p.SW, (int)y, &full[s], p.l2_hint, pol);
+          }
         }
       }
     }
@@ -770,6 +671,93 @@ static cudaError_t encode_fast(const TreesDev& t, const TIn* A, int64_t N, int64
     case 32: return launch_ws_t<TIn, 32, 1, 0, false, true>(tm, p, sf, g.smem, s);
     case 64: return launch_ws_t<TIn, 64, 1, 0, false, true>(tm, p, sf, g.smem, s);
   }
+  *done = false;
+  return cudaSuccess;
+}
+
+// ------------------------------------------------ column-major A --
+// Stage layout [slot][R rows]: one TMA box of {R rows x 1 column} per distinct
+// split column, so only 4 |S| bytes per row leave HBM; an encoder's "row" is
+// stg + r with element offset slot(j) * R for split column j (pitch 1).
+static Geometry plan_cm(int C, int W, int n_cols, bool enc_only) {
+  Geometry g;
+  if (n_cols < 1 || n_cols > 4 * C) return g;
+  g.nslab = n_cols;
+  g.SW = 1;
+  g.pad_e = 0;
+  const int CBW = C >= 8 ? C / 8 : 1;
+  size_t fixed = BAR_BYTES + 16 * C * 4 + 4 * C * 4 + C * 4 + 4 * C * 4 + 16;
+  if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4;
+  fixed = (fixed + 127) & ~size_t(127);
+  const size_t budget = (size_t)dev_info().smem_optin;
+  // Largest R with >= 2 stages: the column boxes are R * 4 bytes and the TMA
+  // rate per box, not the bytes, bounds small boxes (cls100, measured: R = 32 /
+  // 64 / 128 -> 1.2 / 2.2 / 3.5e9 rows/s).
+  const int force_r = env_int("MDN_CM_R", 0);       // experiment knob: fixed rows per stage
+  for (int min_ns : {2}) {
+    for (int R : {256, 128, 64, 32}) {
+      if (force_r && R != force_r) continue;
+      const size_t stage = (size_t)n_cols * R * 4;
+      if (fixed + stage * min_ns > budget) continue;
+      int NS = (int)((budget - fixed) / stage);
+      if (NS > NS_MAX) NS = NS_MAX;
+      g.R = R;
+      g.NS = NS;
+      g.slab_e = R;
+      g.smem = fixed + stage * NS;
+      g.ok = true;
+      return g;
+    }
+  }
+  return g;
+}
+
+static bool make_tmap_cm(CUtensorMap* m, const float* At, int64_t N, int64_t ldt, int D, int R) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)D};
+  cuuint64_t strides[1] = {(cuuint64_t)ldt * 4};
+  cuuint32_t box[2] = {(cuuint32_t)R, 1};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(At), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool cm_ok(const TreesDev& t, const float* At, int64_t N, int64_t ldt) {
+  return N <= (int64_t)0x7FFFFF00 && aligned16(At) && ldt % 4 == 0 && encode_fn() != nullptr &&
+         t.n_cols >= 1;
+}
+
+cudaError_t launch_amm_ws_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
+                             int64_t ldt, float* out, int64_t ldo, cudaStream_t s, bool* done) {
+  *done = false;
+  // Only for heavy scans (W >= 8 table words per code, e.g. M = 100): with
+  // light scans the thread-per-row kernel of mdn_colmajor.cu, whose warps read
+  // the split columns directly, is as fast or faster (scale: 5.5 vs 4.8e9).
+  if (l.W < 8 || !cm_ok(t, At, N, ldt) || !has_combo(t.C, l.W, l.U)) return cudaSuccess;
+  Geometry g = plan_cm(t.C, l.W, t.n_cols, false);
+  if (!g.ok) return cudaSuccess;
+  CUtensorMap tm;
+  if (!make_tmap_cm(&tm, At, N, ldt, t.D, g.R)) return cudaSuccess;
+  Params p = base_params(t, g, N);
+  p.slot = t.slot;
+  p.cols = t.cols;
+  p.ldo = ldo;
+  p.M = l.M;
+  p.pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
+  p.alpha_eff = l.alpha_eff;
+  p.beta32 = l.beta32;
+  p.lut = l.words;
+  p.out = out;
+  const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
+  *done = true;
+#define X(c, w, u)                                                                   \
+  if (t.C == c && l.W == w && l.U == u)                                              \
+    return vec ? launch_ws_sf<float, c, w, u, true, false, CM>(tm, p, g.smem, s)     \
+               : launch_ws_sf<float, c, w, u, false, false, CM>(tm, p, g.smem, s);
+  MDN_FAST_COMBOS(X)
+#undef X
   *done = false;
   return cudaSuccess;
 }

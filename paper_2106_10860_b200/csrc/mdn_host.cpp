@@ -130,6 +130,8 @@ void mdn_model_free(mdn_model* m) {
     cudaFree(m->d_P);
     cudaFree(m->d_sub);
     cudaFree(m->d_q);
+    cudaFree(m->d_cols);
+    cudaFree(m->d_slot);
   }
   delete m;
 }
@@ -192,6 +194,14 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
     double q = std::ceil((double)m->h_thr[i]);
     m->h_q[i] = (uint16_t)(q < 0 ? 0 : (q > 256 ? 256 : q));
   }
+  // Distinct split columns (column-major A reads only these).
+  m->h_slot.assign(D, 0xFFFF);
+  for (size_t i = 0; i < m->h_dims.size(); ++i) m->h_slot[m->h_dims[i]] = 0;
+  for (uint32_t d = 0; d < D; ++d)
+    if (m->h_slot[d] == 0) {
+      m->h_slot[d] = (uint16_t)m->h_cols.size();
+      m->h_cols.push_back((uint16_t)d);
+    }
   m->q_byte = 1;
   for (uint32_t cc = 0; cc < C; ++cc)
     for (int i = 0; i < 15; ++i) m->q_byte &= m->h_q[cc * THR_STRIDE + i] <= 255 ? 1 : 0;
@@ -214,7 +224,9 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   }
   if ((st = dalloc(&m->d_P, (size_t)K * C * D)) != MDN_OK ||
       (st = dalloc(&m->d_sub, (size_t)C)) != MDN_OK ||
-      (st = dalloc(&m->d_q, m->h_q.size())) != MDN_OK) {
+      (st = dalloc(&m->d_q, m->h_q.size())) != MDN_OK ||
+      (st = dalloc(&m->d_cols, m->h_cols.size())) != MDN_OK ||
+      (st = dalloc(&m->d_slot, m->h_slot.size())) != MDN_OK) {
     mdn_model_free(m.release());
     return st;
   }
@@ -223,8 +235,10 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   cudaError_t e3 = cudaMemcpy(m->d_P, P, p_bytes, cudaMemcpyHostToDevice);
   cudaError_t e4 = cudaMemcpy(m->d_sub, m->h_sub.data(), C * 2, cudaMemcpyHostToDevice);
   cudaError_t e5 = cudaMemcpy(m->d_q, m->h_q.data(), m->h_q.size() * 2, cudaMemcpyHostToDevice);
+  cudaError_t e6 = cudaMemcpy(m->d_cols, m->h_cols.data(), m->h_cols.size() * 2, cudaMemcpyHostToDevice);
+  cudaError_t e7 = cudaMemcpy(m->d_slot, m->h_slot.data(), m->h_slot.size() * 2, cudaMemcpyHostToDevice);
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess ||
-      e5 != cudaSuccess) {
+      e5 != cudaSuccess || e6 != cudaSuccess || e7 != cudaSuccess) {
     mdn_model_free(m.release());
     return MDN_ECUDA;
   }
@@ -492,6 +506,30 @@ int mdn_amm_u8(const mdn_model* m, const mdn_luts* l, const uint8_t* A, int64_t 
   if (!g.ok) return MDN_ECUDA;
   return cuda_status(
       launch_amm_u8(m->trees(), l->dev(), A, N, lda, out, ldo, (cudaStream_t)stream));
+}
+
+int mdn_encode_cm(const mdn_model* m, const float* At, int64_t N, int64_t ldt, uint8_t* codes,
+                  void* stream) {
+  if (!m || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!At || !codes || ldt < N) return MDN_EINVAL;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  return cuda_status(launch_encode_cm(m->trees(), At, N, ldt, codes, (cudaStream_t)stream));
+}
+
+int mdn_amm_cm(const mdn_model* m, const mdn_luts* l, const float* At, int64_t N, int64_t ldt,
+               float* out, int64_t ldo, void* stream) {
+  if (!m || !l || N < 0) return MDN_EINVAL;
+  if (l->C != m->C) return MDN_ESHAPE;
+  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  if (l->device != m->device) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!At || !out || ldt < N || ldo < l->M) return MDN_EINVAL;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  return cuda_status(
+      launch_amm_cm(m->trees(), l->dev(), At, N, ldt, out, ldo, (cudaStream_t)stream));
 }
 
 int mdn_amm_variant(const mdn_model* m, const mdn_luts* l, int64_t lda, char* buf, size_t len) {

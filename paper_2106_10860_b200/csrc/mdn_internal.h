@@ -28,6 +28,9 @@ struct TreesDev {
   int subf;              // fp32: 1 / 2 = every subspace 16-B aligned and <= 4 / 8 wide
   int subf_u8;           // uint8: 1 / 2 = every subspace exactly 4 / 8 bytes, contiguous
   int q_byte;            // every 8-bit split value q <= 255 (fits a byte)
+  const uint16_t* cols;  // distinct split columns, ascending [n_cols] (column-major A)
+  const uint16_t* slot;  // [D] index of each split column in `cols` (0xFFFF otherwise)
+  int n_cols;
 };
 
 // Quantised tables as the kernels consume them (device).
@@ -60,6 +63,16 @@ cudaError_t launch_amm_rt(const TreesDev& t, const LutsDev& l, const float* A, i
 cudaError_t launch_amm_rt_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
                              int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done);
 bool amm_rt_applies(const TreesDev& t, const LutsDev& l, int es);
+// Column-major A (mdn_colmajor.cu).
+cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
+                          int64_t ldt, float* out, int64_t ldo, cudaStream_t s);
+cudaError_t launch_encode_cm(const TreesDev& t, const float* At, int64_t N, int64_t ldt,
+                             uint8_t* codes, cudaStream_t s);
+// Warp-specialised TMA variant of the fused path for column-major A with heavy
+// scans (mdn_fast.cu); *done = false when not applicable (the caller then uses
+// mdn_colmajor.cu's thread-per-row kernel).
+cudaError_t launch_amm_ws_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
+                             int64_t ldt, float* out, int64_t ldo, cudaStream_t s, bool* done);
 const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
                              const float* out, int64_t ldo);
 
@@ -92,12 +105,17 @@ struct mdn_model {
   std::vector<uint16_t> h_sub;    // [C] subspace begin
   std::vector<uint16_t> h_q;      // [C][16] 8-bit split values
   int subf = 0, subf_u8 = 0, q_byte = 0;
+  std::vector<uint16_t> h_cols, h_slot;
+  uint16_t* d_cols = nullptr;
+  uint16_t* d_slot = nullptr;
   uint16_t* d_dims = nullptr;
   float* d_thr = nullptr;
   uint16_t* d_sub = nullptr;
   uint16_t* d_q = nullptr;
   float* d_P = nullptr;           // [16C][D]
-  mdn::TreesDev trees() const { return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8, q_byte}; }
+  mdn::TreesDev trees() const {
+    return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8, q_byte, d_cols, d_slot, (int)h_cols.size()};
+  }
 };
 
 struct mdn_luts {

@@ -1,0 +1,136 @@
+// Scan core shared by the TMA-fed fused kernel (mdn_fast.cu) and the
+// column-major kernel (mdn_colmajor.cu): table lookups of 32-bit words holding
+// 4 output columns, exact 16-bit SWAR sums or the App. D averaging tree, and
+// the dequantising row store.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mdn {
+namespace fast {
+
+// ------------------------------------------------------------ scan core --
+
+// Accumulate the W table words of every codebook for one row.
+//   words(g): the g-th 32-bit word of the row's packed codes (8 codes, low
+//   nibble first; for C < 8 only the low 4C bits are used).
+// Exact mode (U == 0): ae[w] / ao[w] hold the even / odd output columns of
+// word w in two 16-bit lanes (S <= 255 C < 2^16 for C <= 256).
+// Averaging mode: per block of U consecutive codebooks the halves-recursion
+// tree of rounded averages (mu(a,b) = (a+b+1)>>1 per byte, avg8), and the
+// block results are summed exactly (App. D, reading R16/R17).
+// mu(a, b) = floor((a + b + 1) / 2) on 4 byte lanes (App. D) as
+// (a | b) - (((a ^ b) & 0xFE..) >> 1): per byte a | b = (a & b) + (a ^ b) can
+// never borrow, and the mask keeps each byte's low bit from shifting into its
+// neighbour. 4 ALU ops (LOP3, LOP3, SHF, IADD) against 5 for __vavgu4.
+__device__ __forceinline__ uint32_t avg8(uint32_t a, uint32_t b) {
+  uint32_t x;   // (a ^ b) & 0xFEFEFEFE in one LOP3 (inline: LLVM would re-canonicalise it)
+  asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(x) : "r"(a), "r"(b), "r"(0xFEFEFEFEu));
+  return (a | b) - (x >> 1);
+}
+
+template <int C, int W, int U, bool UNROLL_G = false, class Words>
+__device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Words words,
+                                          uint32_t (&ae)[W], uint32_t (&ao)[W]) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) ae[w] = ao[w] = 0u;
+  if constexpr (U == 0) {
+    constexpr int G = C >= 8 ? 8 : C;
+    constexpr int NGU = UNROLL_G ? C / G : 1;
+#pragma unroll NGU
+    for (int g = 0; g < C / G; ++g) {
+      const uint32_t cw = words(g);
+      const uint32_t* lg = lut + g * G * W * 16;
+#pragma unroll
+      for (int i = 0; i < G; i += 2) {
+        const uint32_t* p0 = lg + (i * W) * 16 + ((cw >> (4 * i)) & 15u);
+        const uint32_t* p1 = lg + ((i + 1) * W) * 16 + ((cw >> (4 * i + 4)) & 15u);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const uint32_t a = p0[w * 16], b = p1[w * 16];
+          ae[w] += (a & 0x00FF00FFu) + (b & 0x00FF00FFu);
+          ao[w] += __byte_perm(a, 0u, 0x4341) + __byte_perm(b, 0u, 0x4341);
+        }
+      }
+    }
+  } else {
+    static_assert((U & (U - 1)) == 0 && C % U == 0, "U must be a power of two dividing C");
+    constexpr int NBU = UNROLL_G ? C / U : 1;
+#pragma unroll NBU
+    for (int blk = 0; blk < C / U; ++blk) {
+      const uint32_t* p[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const int c = blk * U + i;  // runtime blk, static i
+        uint32_t cw;
+        if constexpr (U >= 8) {
+          cw = words(blk * (U / 8) + i / 8);
+          p[i] = lut + (c * W) * 16 + ((cw >> (4 * (i % 8))) & 15u);
+        } else {
+          const int cc = blk * U + i;
+          cw = words(cc >> 3);
+          p[i] = lut + (c * W) * 16 + ((cw >> (4 * (cc & 7))) & 15u);
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint32_t v[U];
+#pragma unroll
+        for (int i = 0; i < U; ++i) v[i] = p[i][w * 16];
+#pragma unroll
+        for (int s = 1; s < U; s *= 2)
+#pragma unroll
+          for (int i = 0; i < U; i += 2 * s) v[i] = avg8(v[i], v[i + s]);
+        ae[w] += v[0] & 0x00FF00FFu;
+        ao[w] += __byte_perm(v[0], 0u, 0x4341);
+      }
+    }
+  }
+}
+
+// out[m] = fl32(alpha_eff * S'[m] + beta32): S' < 2^16 is exact in fp32 and
+// alpha_eff a power of two, so the FMA's single rounding equals the oracle's.
+// pair: (non-VEC) M even and the row 8-byte aligned -> 8-byte stores.
+template <int W, bool VEC>
+__device__ __forceinline__ void store_row(float* __restrict__ o, int M, const uint32_t (&ae)[W],
+                                          const uint32_t (&ao)[W], float a, float b,
+                                          bool pair = false) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    float4 f;
+    f.x = __fmaf_rn(a, (float)(ae[w] & 0xFFFFu), b);
+    f.y = __fmaf_rn(a, (float)(ao[w] & 0xFFFFu), b);
+    f.z = __fmaf_rn(a, (float)(ae[w] >> 16), b);
+    f.w = __fmaf_rn(a, (float)(ao[w] >> 16), b);
+    if constexpr (VEC) {
+      *reinterpret_cast<float4*>(o + 4 * w) = f;
+    } else if (pair) {
+      const int m = 4 * w;
+      if (m + 1 < M) *reinterpret_cast<float2*>(o + m) = make_float2(f.x, f.y);
+      if (m + 3 < M) *reinterpret_cast<float2*>(o + m + 2) = make_float2(f.z, f.w);
+    } else {
+      const int m = 4 * w;
+      if (m + 0 < M) o[m + 0] = f.x;
+      if (m + 1 < M) o[m + 1] = f.y;
+      if (m + 2 < M) o[m + 2] = f.z;
+      if (m + 3 < M) o[m + 3] = f.w;
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void store_sums(int32_t* __restrict__ o, int M, int scale,
+                                           const uint32_t (&ae)[W], const uint32_t (&ao)[W]) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const int m = 4 * w;
+    const int v[4] = {(int)(ae[w] & 0xFFFFu), (int)(ao[w] & 0xFFFFu), (int)(ae[w] >> 16),
+                      (int)(ao[w] >> 16)};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (m + i < M) o[m + i] = v[i] * scale;
+  }
+}
+
+}  // namespace fast
+}  // namespace mdn

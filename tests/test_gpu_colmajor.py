@@ -1,0 +1,111 @@
+"""GPU parity of the column-major path:
+mdn_encode_cm / mdn_amm_cm on At = A^T against the oracle's encode / amm on
+the same A (the oracle's definition of g does not depend on the storage order).
+Codes and fp32 outputs bit-exact."""
+import numpy as np
+import pytest
+
+import oracle as O
+from datagen.synth import CONFIGS, relu_W, relu_lowrank_torch
+from test_gpu_parity import MODES, _assert_out, _setup
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mdn():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2106_10860_b200 as m
+    return m
+
+
+def _At(A, pad=0):
+    """A^T on the device, D x N with row stride N + pad."""
+    N, D = A.shape
+    big = torch.zeros((D, N + pad), device="cuda")
+    big[:, :N] = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+    return big[:, :N]
+
+
+CFGS = ["tiny", "cls10_c16", "cls10_c64", "cls100", "image", "scale"]
+
+
+@pytest.mark.parametrize("name", CFGS)
+def test_encode_cm_bit_exact(mdn, name):
+    model, om, A, B = _setup(mdn, name)
+    A = A[:50_000]
+    codes = torch.empty((A.shape[0], (om.C + 1) // 2), dtype=torch.uint8, device="cuda")
+    mdn.mdn_encode_cm(model, _At(A), codes)
+    want = O.pack_codes(O.encode(A, om))
+    got = codes.cpu().numpy()
+    assert (got == want).all(), f"{(got != want).sum()} code bytes differ"
+
+
+@pytest.mark.parametrize("name", CFGS)
+@pytest.mark.parametrize("mode", MODES, ids=["exact", "avg"])
+def test_amm_cm_bit_exact(mdn, name, mode):
+    model, om, A, B = _setup(mdn, name)
+    A = A[:50_000]
+    spec = CONFIGS[name]
+    luts = mdn.mdn_build_luts(model, B, mode[1], spec.U)
+    want = O.amm(A, om, O.make_luts(om, B, mode[0], spec.U))[2]
+    out = torch.full((A.shape[0], spec.M), float("nan"), device="cuda")
+    mdn.mdn_amm_cm(model, luts, _At(A), out)
+    _assert_out(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("N", [1, 31, 257, 4099])
+def test_cm_ragged_strided(mdn, N):
+    """Ragged N, ldt > N (padded columns), ldo > M (paired / scalar stores)."""
+    model, om, A, B = _setup(mdn, "cls10_c32")
+    luts = mdn.mdn_build_luts(model, B, 1, 16)
+    A = A[:N]
+    want = O.amm(A, om, O.make_luts(om, B, "avg", 16))[2]
+    outbig = torch.zeros((N, 13), device="cuda")
+    out = outbig[:, :10]
+    mdn.mdn_amm_cm(model, luts, _At(A, pad=5), out)
+    _assert_out(out.cpu().numpy(), want)
+    codes = torch.empty((N, 16), dtype=torch.uint8, device="cuda")
+    mdn.mdn_encode_cm(model, _At(A, pad=3), codes)
+    assert (codes.cpu().numpy() == O.pack_codes(O.encode(A, om))).all()
+
+
+def test_cm_errors(mdn):
+    model, om, A, B = _setup(mdn, "tiny")
+    luts = mdn.mdn_build_luts(model, B, 0)
+    At = _At(A[:100])
+    out = torch.empty((100, 4), device="cuda")
+    with pytest.raises(ValueError):
+        mdn.mdn_amm_cm(model, luts, At.t(), out)            # not D x N
+    # ldt < N is refused by the library itself
+    import paper_2106_10860_b200 as m
+    st = m._lib.mdn_amm_cm(model._h, luts._h, At.data_ptr(), 100, 50, out.data_ptr(), 4, None)
+    assert st == -1
+    mdn.mdn_amm_cm(model, luts, At[:, :0], out[:0])           # N = 0 is a no-op
+
+
+def test_cm_bench_size_sampled_parity(mdn):
+    """cls100 at the bench size (2^21 rows, At 4 GiB) as bench.py --layout col
+    launches it; 65536 sampled rows + the tail against the oracle."""
+    name, n_rows = "cls100", 1 << 21
+    spec = CONFIGS[name]
+    model, om, _, B = _setup(mdn, name)
+    A = relu_lowrank_torch(relu_W(name), n_rows, 0, "cuda")
+    At = A.t().contiguous()
+    rng = np.random.default_rng(321)
+    rows = np.unique(np.concatenate([rng.integers(0, n_rows, 65536), np.arange(n_rows - 300, n_rows)]))
+    idx = torch.from_numpy(rows).cuda()
+    As = A.index_select(0, idx).cpu().numpy()
+    del A
+    for mode, mi in MODES:
+        luts = mdn.mdn_build_luts(model, B, mi, spec.U)
+        out = torch.empty((n_rows, spec.M), device="cuda")
+        mdn.mdn_amm_cm(model, luts, At, out)
+        torch.cuda.synchronize()
+        got = out.index_select(0, idx).cpu().numpy()
+        _assert_out(got, O.amm(As, om, O.make_luts(om, B, mode, spec.U))[2])
+        del out
+    del At
+    torch.cuda.empty_cache()
