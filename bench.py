@@ -431,7 +431,7 @@ def run(args):
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(f"{name}_{args.mode}")
+                traffic = json.load(open(tp)).get(f"{name}{'_col' if col else ''}_{args.mode}")
             except Exception:
                 traffic = None
         line = {
