@@ -259,7 +259,9 @@ def run(args):
     # --- model + LUTs: built once on rank 0, broadcast as bytes over NCCL -----
     t_bcast = 0.0
     if rank == 0:
-        model_blob = open(os.path.join(ROOT, "artifacts", f"{name}.mdnm"), "rb").read()
+        pq = args.encoder == "pq"
+        model_blob = open(os.path.join(ROOT, "artifacts", f"{name}{'_pq' if pq else ''}.mdnm"),
+                          "rb").read()
         B = _config_B(name)
         m0 = mdn.mdn_model_load(model_blob, dev)
         l0 = mdn.mdn_build_luts(m0, B, mode, spec.U)
@@ -280,15 +282,25 @@ def run(args):
     torch.cuda.synchronize()
 
     op = args.op
-    codes = None
-    if op != "amm":
-        codes = torch.empty((n, (spec.C + 1) // 2), dtype=torch.uint8, device="cuda")
-        (mdn.mdn_encode_u8 if A.dtype == torch.uint8 else mdn.mdn_encode)(model, A, codes)
-        torch.cuda.synchronize()
-
+    pq = args.encoder == "pq"
     u8 = A.dtype == torch.uint8
     amm_fn = mdn.mdn_amm_u8 if u8 else mdn.mdn_amm
     enc_fn = mdn.mdn_encode_u8 if u8 else mdn.mdn_encode
+    codes = None
+    if pq:
+        # PQ comparator: g = nearest of 16 K-means prototypes per
+        # subspace; "amm" = PQ encode + the same scan (two launches per step).
+        assert not u8 and args.layout == "row", "--encoder pq: fp32 row-major A"
+        enc_fn = mdn.mdn_encode_pq
+        codes = torch.empty((n, (spec.C + 1) // 2), dtype=torch.uint8, device="cuda")
+
+        def amm_fn(m, l, A_, o, stream=None):
+            mdn.mdn_encode_pq(m, A_, codes, stream=stream)
+            mdn.mdn_scan(l, codes, out=o, stream=stream)
+    if op != "amm":
+        codes = torch.empty((n, (spec.C + 1) // 2), dtype=torch.uint8, device="cuda")
+        enc_fn(model, A, codes)
+        torch.cuda.synchronize()
     col = args.layout == "col"
     if col:
         # Column-major A: the same rows stored as At = A^T (D x N).
@@ -339,7 +351,7 @@ def run(args):
     # Achievable-bandwidth probe: a plain streaming kernel with the same byte
     # mix (read A, write M floats per row), timed the same way.
     probe = None
-    if op == "amm" and not u8 and not col and spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
+    if op == "amm" and not u8 and not col and not pq and spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
         probe_out = torch.empty_like(out)     # never overwrite the step's output
         for _ in range(2):
             mdn.mdn_stream_probe(A, probe_out, stream=stream)
@@ -357,6 +369,26 @@ def run(args):
     peak, peak_kind = _peaks()
     avg_launch_s = statistics.mean(per_launch) / 1e3
     achieved_gbs = n * bytes_per_row / avg_launch_s / 1e9
+    pq_roof = None
+    if pq:
+        # The PQ encoder is bound by the fp32 pipe, not HBM: 16 prototypes x D
+        # dims x (subtract, multiply, add) per row (Eq. pqLoss, no FMA).
+        # Peak (derived): 148 SMs x 128 fp32 lanes x 1 op/clk x max clock.
+        pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.cuda.synchronize()
+        pe[0].record(stream)
+        for _ in range(args.steps):
+            mdn.mdn_encode_pq(model, A, codes, stream=stream)
+        pe[1].record(stream)
+        torch.cuda.synchronize()
+        t_enc = pe[0].elapsed_time(pe[1]) / 1e3 / args.steps
+        sm_mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
+        fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+        tflops = n * 48 * spec.D / t_enc / 1e12
+        pq_roof = {"bound": "fp32", "achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+                   "frac": tflops / fp32_peak, "peak_kind": "derived: 148 SMs x 128 fp32 lanes x clock",
+                   "traffic": None, "algorithmic_flops_per_launch": n * 48 * spec.D,
+                   "kernel": "k_encode_pq", "encode_rows_per_s": n / t_enc}
 
     # --- quality (NMSE vs exact fp64 AB on 65536 rows) and the cuBLAS context point
     nmse = None
@@ -384,7 +416,7 @@ def run(args):
 
     # --- e2e: the same metric through the public API with HOST buffers --------
     e2e = None
-    if op == "amm" and not u8 and not col and (rank == 0 or ws > 1):
+    if op == "amm" and not u8 and not col and not pq and (rank == 0 or ws > 1):
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
                                  n_slots=3)
         n_e2e = min(n, (1 << 32) // (4 * spec.D))     # <= 4 GiB of pinned host A per rank
@@ -409,7 +441,7 @@ def run(args):
 
     # --- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only ---
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and op == "amm" and not col:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and op == "amm" and not col and not pq:
         import oracle as O
         om = O.read_model(model_blob)
         oluts = O.make_luts(om, B, args.mode, spec.U)
@@ -436,7 +468,8 @@ def run(args):
                 traffic = None
         line = {
             "metric": _metric(name) + ("" if op == "amm" else f" [{op} only]")
-                      + (" [column-major A]" if col else ""), "value": value,
+                      + (" [column-major A]" if col else "") + (" [PQ encoder]" if pq else ""),
+            "value": value,
             "unit": "rows/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
@@ -444,24 +477,25 @@ def run(args):
             "config": {"workload": f"{name}: D={spec.D}, M={spec.M}, C={spec.C}, K=16, {args.mode} sum"
                        + (f" (U={spec.U})" if args.mode == "avg" else "")
                        + ("; relu low-rank rows" if spec.kind == "relu" else "; 3x3x3 image patches")
-                       + ", oracle-trained trees / ridge prototypes"
+                       + (", PQ comparator: oracle K-means prototypes, encode = nearest prototype"
+                          if pq else ", oracle-trained trees / ridge prototypes")
                        + ("; A stored column-major (At = A^T), only the split columns read" if col else ""),
                        "rows_per_gpu": n, "global_rows_per_step": n * ws,
                        "A_bytes_per_gpu": n * 4 * spec.D,
                        "l2": f"inputs {n * 4 * spec.D / 2**30:.1f} GiB per GPU > 126 MB L2; no flush",
                        "parallelism": f"row-sharded dp{ws}, model+LUT NCCL broadcast once"},
             "pct_hbm_nominal_8tbs": achieved_gbs / NOMINAL_HBM_GBS,
-            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+            "roofline": pq_roof or {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "peak_kind": peak_kind,
                          "traffic": traffic,
                          "algorithmic_bytes_per_launch": n * bytes_per_row,
-                         "kernel": ("k_amm_cm" if col else mdn.mdn_amm_variant(model, luts, spec.D))
+                         "kernel": ("k_amm_cm" if col else ("pq" if pq else mdn.mdn_amm_variant(model, luts, spec.D)))
                                    if op == "amm" else op,
                          "frac_of_stream_probe": (achieved_gbs / probe["gbs"]) if probe else None},
             "stream_probe": probe,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * (2 if pq and op == "amm" else 1),
             "op": op,
             "clocks": clocks,
             "nmse_vs_exact_fp64": nmse,
@@ -487,6 +521,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--op", choices=["amm", "encode", "scan"], default="amm",
                     help="amm (the hot path, default) or the unfused halves, for DESIGN.md")
+    ap.add_argument("--encoder", choices=["maddness", "pq"], default="maddness",
+                    help="maddness (the method) or pq: the PQ comparator encoder (SURVEY N4) "
+                         "feeding the same scan")
     ap.add_argument("--layout", choices=["row", "col"], default="row",
                     help="row-major A (default) or column-major A (SURVEY N2: split-column gather)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -169,6 +169,21 @@ int mdn_encode_cm(const mdn_model* model, const float* At, int64_t N, int64_t ld
 int mdn_amm_cm(const mdn_model* model, const mdn_luts* luts, const float* At, int64_t N,
                int64_t ldt, float* out, int64_t ldo, void* stream);
 
+/* --------------------------------------------- PQ comparator -- */
+
+/* g(A) of Product Quantization, the encoder MADDNESS replaces (PAPER.md Sec.
+ * 3, Eq. pqLoss): per codebook the index of the nearest of the 16
+ * K-means prototypes (L155-163) in squared Euclidean distance over the
+ * codebook's subspace, evaluated in fp32 with every subtract / multiply / add
+ * rounded separately, dims ascending; ties go to the lowest index.
+ *   model  a PQ model: "model.mdnm" with flags bit1 set; its P holds the
+ *          prototypes (row 16c + k, zero outside subspace c). MDN_ESTATE for
+ *          a MADDNESS model (and the tree-based calls refuse PQ models).
+ *   A, codes as mdn_encode. The codes feed mdn_scan with tables from
+ *   mdn_build_luts(model, B, ...) exactly like MADDNESS codes. */
+int mdn_encode_pq(const mdn_model* model, const float* A, int64_t N, int64_t lda,
+                  uint8_t* codes, void* stream);
+
 /* ----------------------------------------------------- end-to-end (host) -- */
 
 /* A pipelined executor for HOST buffers: row chunks are copied host->device,
@@ -208,7 +223,8 @@ int mdn_amm_variant(const mdn_model* model, const mdn_luts* luts, int64_t lda,
  * library share; each side has its own reader/writer.
  *
  * model.mdnm v1
- *   char[4] "MDNM" | u32 ver = 1 | u32 C | u32 D | u32 K = 16 | u32 flags (bit0 ridge)
+ *   char[4] "MDNM" | u32 ver = 1 | u32 C | u32 D | u32 K = 16 | u32 flags (bit0 ridge,
+ *   bit1 PQ model: P = K-means prototypes, tree fields unused)
  *   f64 lambda | u64 n_train | u64 seed
  *   C records: u32 sub_begin | u32 sub_end | u16 dim[4] | f32 thr[15]
  *              (thr in heap order: level t node p at 2^t - 1 + p)

@@ -20,3 +20,4 @@ the figures are missing) -- "parity unpinned" for that quantity only.
 """
 from .maddness import *  # noqa: F401,F403
 from .model_file import read_model, write_model  # noqa: F401
+from .pq import amm_pq, encode_pq, kmeans, pq_distances, train_pq  # noqa: F401

@@ -58,6 +58,7 @@ class Model:
     seed: int = 0
     ridge: bool = True
     level_losses: list = field(default_factory=list)   # per codebook, 4 floats
+    pq: bool = False     # PQ comparator model (oracle/pq.py): P = K-means prototypes, no trees
 
 
 # ---------------------------------------------------------------------------

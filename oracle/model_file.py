@@ -4,7 +4,8 @@ The byte layout is the documented contract in ``include/maddness.h``
 (section "model.mdnm v1"); the library has its own independent parser.
 All fields little-endian:
 
-  "MDNM" | u32 ver=1 | u32 C | u32 D | u32 K=16 | u32 flags (bit0 = ridge)
+  "MDNM" | u32 ver=1 | u32 C | u32 D | u32 K=16 | u32 flags (bit0 = ridge,
+                                                            bit1 = PQ model)
   f64 lambda | u64 n_train | u64 seed
   C x { u32 sub_begin | u32 sub_end | u16 dim[4] | f32 thr[15] }
   f32 P[16C][D]
@@ -25,7 +26,8 @@ VERSION = 1
 def write_model(model: Model) -> bytes:
     out = bytearray()
     out += MAGIC
-    out += struct.pack("<5I", VERSION, model.C, model.D, K, 1 if model.ridge else 0)
+    flags = (1 if model.ridge else 0) | (2 if getattr(model, "pq", False) else 0)
+    out += struct.pack("<5I", VERSION, model.C, model.D, K, flags)
     out += struct.pack("<dQQ", float(model.lam), int(model.n_train), int(model.seed))
     for c in range(model.C):
         b, e = model.sub[c]
@@ -71,4 +73,4 @@ def read_model(buf: bytes) -> Model:
     if fp != fnv1a64(buf[:off]):
         raise ValueError("fingerprint mismatch")
     return Model(C=C, D=D, sub=sub, dims=dims, thr=thr, P=P, lam=lam,
-                 n_train=n_train, seed=seed, ridge=bool(flags & 1))
+                 n_train=n_train, seed=seed, ridge=bool(flags & 1), pq=bool(flags & 2))

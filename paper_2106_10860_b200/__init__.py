@@ -57,6 +57,7 @@ _SIGS = {
     "mdn_amm_u8": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "mdn_encode_cm": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "mdn_amm_cm": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "mdn_encode_pq": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -244,6 +245,18 @@ def mdn_amm_u8(model: Model, luts: Luts, A, out, stream=None):
     _check(_lib.mdn_amm_u8(model._h, luts._h, pa, A.shape[0], A.stride(0), po, out.stride(0),
                            _stream_ptr(stream)), "mdn_amm_u8")
     return out
+
+
+def mdn_encode_pq(model: Model, A, codes, stream=None):
+    """g(A) of the PQ comparator (SURVEY N4, PAPER.md Eq. pqLoss L182-184);
+    `model` must be a PQ model (flags bit1)."""
+    pa = _dev_ptr(A, "float32", "A")
+    pc = _dev_ptr(codes, "uint8", "codes")
+    if codes.shape != (A.shape[0], (model.C + 1) // 2) or not codes.is_contiguous():
+        raise ValueError("codes must be contiguous N x ceil(C/2)")
+    _check(_lib.mdn_encode_pq(model._h, pa, A.shape[0], A.stride(0), pc, _stream_ptr(stream)),
+           "mdn_encode_pq")
+    return codes
 
 
 def _colmajor(At, what):

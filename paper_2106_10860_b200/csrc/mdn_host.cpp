@@ -132,6 +132,8 @@ void mdn_model_free(mdn_model* m) {
     cudaFree(m->d_q);
     cudaFree(m->d_cols);
     cudaFree(m->d_slot);
+    cudaFree(m->d_sub_e);
+    cudaFree(m->d_pqcent);
   }
   delete m;
 }
@@ -160,12 +162,15 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   m->h_dims.assign((size_t)C * 4, 0);
   m->h_thr.assign((size_t)C * THR_STRIDE, 0.f);
   m->h_sub.assign(C, 0);
+  m->h_sub_e.assign(C, 0);
+  m->pq = (flags & 2u) != 0;
   int max_w = 0;
   bool aligned = true;
   for (uint32_t c = 0; c < C; ++c) {
     size_t rec = r.off;
     uint32_t b = r.get<uint32_t>(), e = r.get<uint32_t>();
     m->h_sub[c] = (uint16_t)b;
+    m->h_sub_e[c] = (uint16_t)e;
     if ((int)(e - b) > max_w) max_w = (int)(e - b);
     if (b % 4) aligned = false;
     for (int t = 0; t < 4; ++t) m->h_dims[c * 4 + t] = r.get<uint16_t>();
@@ -213,6 +218,28 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   uint64_t fp = fnv1a64(r.p, r.off - 8);
   if (fp != fp_stored) return set_err(err_off, r.off - 8, MDN_EFORMAT);
   m->fingerprint = fp;
+  // PQ model (flags bit1): prototypes re-laid out [16][DS/4][C][4]
+  // for the fast encoder when every subspace is [c DS, (c+1) DS), DS in
+  // {4, 8, 16, 32} and C divides 256 (else the generic PQ kernel reads P).
+  std::vector<float> h_pqcent;
+  if (m->pq) {
+    const int DS = (int)(D / C);
+    bool eq = (int)D == DS * (int)C && (DS == 4 || DS == 8 || DS == 16 || DS == 32) &&
+              256 % C == 0 && C % 2 == 0;
+    for (uint32_t cc = 0; cc < C && eq; ++cc) eq = m->h_sub[cc] == DS * cc && m->h_sub_e[cc] == DS * (cc + 1);
+    if (eq) {
+      m->pq_ds = DS;
+      h_pqcent.resize((size_t)16 * D);
+      const float* Pf = reinterpret_cast<const float*>(P);
+      for (int k = 0; k < 16; ++k)
+        for (int j = 0; j < DS; ++j)
+          for (uint32_t cc = 0; cc < C; ++cc) {
+            float v;
+            memcpy(&v, reinterpret_cast<const uint8_t*>(Pf) + (((size_t)(16 * cc + k) * D + cc * DS + j) * 4), 4);
+            h_pqcent[(((size_t)k * (DS / 4) + j / 4) * C + cc) * 4 + (j % 4)] = v;
+          }
+    }
+  }
 
   DeviceGuard g(device);
   if (!g.ok) return MDN_ECUDA;
@@ -226,7 +253,9 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
       (st = dalloc(&m->d_sub, (size_t)C)) != MDN_OK ||
       (st = dalloc(&m->d_q, m->h_q.size())) != MDN_OK ||
       (st = dalloc(&m->d_cols, m->h_cols.size())) != MDN_OK ||
-      (st = dalloc(&m->d_slot, m->h_slot.size())) != MDN_OK) {
+      (st = dalloc(&m->d_slot, m->h_slot.size())) != MDN_OK ||
+      (st = dalloc(&m->d_sub_e, (size_t)C)) != MDN_OK ||
+      (!h_pqcent.empty() && (st = dalloc(&m->d_pqcent, h_pqcent.size())) != MDN_OK)) {
     mdn_model_free(m.release());
     return st;
   }
@@ -237,8 +266,13 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   cudaError_t e5 = cudaMemcpy(m->d_q, m->h_q.data(), m->h_q.size() * 2, cudaMemcpyHostToDevice);
   cudaError_t e6 = cudaMemcpy(m->d_cols, m->h_cols.data(), m->h_cols.size() * 2, cudaMemcpyHostToDevice);
   cudaError_t e7 = cudaMemcpy(m->d_slot, m->h_slot.data(), m->h_slot.size() * 2, cudaMemcpyHostToDevice);
+  cudaError_t e8 = cudaMemcpy(m->d_sub_e, m->h_sub_e.data(), C * 2, cudaMemcpyHostToDevice);
+  cudaError_t e9 = h_pqcent.empty() ? cudaSuccess
+                                    : cudaMemcpy(m->d_pqcent, h_pqcent.data(), h_pqcent.size() * 4,
+                                                 cudaMemcpyHostToDevice);
   if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess ||
-      e5 != cudaSuccess || e6 != cudaSuccess || e7 != cudaSuccess) {
+      e5 != cudaSuccess || e6 != cudaSuccess || e7 != cudaSuccess || e8 != cudaSuccess ||
+      e9 != cudaSuccess) {
     mdn_model_free(m.release());
     return MDN_ECUDA;
   }
@@ -454,6 +488,7 @@ int mdn_luts_info(const mdn_luts* l, int* C, int* M, int* mode, int* U, int* lex
 int mdn_encode(const mdn_model* m, const float* A, int64_t N, int64_t lda, uint8_t* codes,
                void* stream) {
   if (!m || N < 0) return MDN_EINVAL;
+  if (m->pq) return MDN_ESTATE;              // PQ model: no hash trees (mdn_encode_pq)
   if (N == 0) return MDN_OK;
   if (!A || !codes || lda < m->D) return MDN_EINVAL;
   DeviceGuard g(m->device);
@@ -475,7 +510,7 @@ int mdn_amm(const mdn_model* m, const mdn_luts* l, const float* A, int64_t N, in
             float* out, int64_t ldo, void* stream) {
   if (!m || !l || N < 0) return MDN_EINVAL;
   if (l->C != m->C) return MDN_ESHAPE;
-  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  if (l->model_fp != m->fingerprint || m->pq) return MDN_ESTATE;
   if (l->device != m->device) return MDN_EINVAL;
   if (N == 0) return MDN_OK;
   if (!A || !out || lda < m->D || ldo < l->M) return MDN_EINVAL;
@@ -487,6 +522,7 @@ int mdn_amm(const mdn_model* m, const mdn_luts* l, const float* A, int64_t N, in
 int mdn_encode_u8(const mdn_model* m, const uint8_t* A, int64_t N, int64_t lda, uint8_t* codes,
                   void* stream) {
   if (!m || N < 0) return MDN_EINVAL;
+  if (m->pq) return MDN_ESTATE;              // PQ model: no hash trees (mdn_encode_pq)
   if (N == 0) return MDN_OK;
   if (!A || !codes || lda < m->D) return MDN_EINVAL;
   DeviceGuard g(m->device);
@@ -498,7 +534,7 @@ int mdn_amm_u8(const mdn_model* m, const mdn_luts* l, const uint8_t* A, int64_t 
                float* out, int64_t ldo, void* stream) {
   if (!m || !l || N < 0) return MDN_EINVAL;
   if (l->C != m->C) return MDN_ESHAPE;
-  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  if (l->model_fp != m->fingerprint || m->pq) return MDN_ESTATE;
   if (l->device != m->device) return MDN_EINVAL;
   if (N == 0) return MDN_OK;
   if (!A || !out || lda < m->D || ldo < l->M) return MDN_EINVAL;
@@ -508,9 +544,22 @@ int mdn_amm_u8(const mdn_model* m, const mdn_luts* l, const uint8_t* A, int64_t 
       launch_amm_u8(m->trees(), l->dev(), A, N, lda, out, ldo, (cudaStream_t)stream));
 }
 
+int mdn_encode_pq(const mdn_model* m, const float* A, int64_t N, int64_t lda, uint8_t* codes,
+                  void* stream) {
+  if (!m || N < 0) return MDN_EINVAL;
+  if (!m->pq) return MDN_ESTATE;              // not a PQ model (flags bit1)
+  if (N == 0) return MDN_OK;
+  if (!A || !codes || lda < m->D) return MDN_EINVAL;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  return cuda_status(launch_encode_pq(m->trees(), m->d_P, m->d_sub, m->d_sub_e, A, N, lda, codes,
+                                      (cudaStream_t)stream));
+}
+
 int mdn_encode_cm(const mdn_model* m, const float* At, int64_t N, int64_t ldt, uint8_t* codes,
                   void* stream) {
   if (!m || N < 0) return MDN_EINVAL;
+  if (m->pq) return MDN_ESTATE;              // PQ model: no hash trees (mdn_encode_pq)
   if (N == 0) return MDN_OK;
   if (!At || !codes || ldt < N) return MDN_EINVAL;
   DeviceGuard g(m->device);
@@ -522,7 +571,7 @@ int mdn_amm_cm(const mdn_model* m, const mdn_luts* l, const float* At, int64_t N
                float* out, int64_t ldo, void* stream) {
   if (!m || !l || N < 0) return MDN_EINVAL;
   if (l->C != m->C) return MDN_ESHAPE;
-  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  if (l->model_fp != m->fingerprint || m->pq) return MDN_ESTATE;
   if (l->device != m->device) return MDN_EINVAL;
   if (N == 0) return MDN_OK;
   if (!At || !out || ldt < N || ldo < l->M) return MDN_EINVAL;
@@ -578,7 +627,7 @@ int mdn_exec_create(const mdn_model* m, const mdn_luts* l, int64_t chunk_rows, i
                     mdn_exec** out) {
   if (!m || !l || !out || chunk_rows < 1 || n_slots < 1 || n_slots > 8) return MDN_EINVAL;
   if (l->C != m->C) return MDN_ESHAPE;
-  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  if (l->model_fp != m->fingerprint || m->pq) return MDN_ESTATE;
   *out = nullptr;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;

@@ -31,6 +31,8 @@ struct TreesDev {
   const uint16_t* cols;  // distinct split columns, ascending [n_cols] (column-major A)
   const uint16_t* slot;  // [D] index of each split column in `cols` (0xFFFF otherwise)
   int n_cols;
+  const float* pq_cent;  // PQ model: prototypes [16][DS/4][C][4] (equal subspaces), or null
+  int pq_ds;             // PQ subspace width DS of pq_cent (0 if null)
 };
 
 // Quantised tables as the kernels consume them (device).
@@ -63,6 +65,10 @@ cudaError_t launch_amm_rt(const TreesDev& t, const LutsDev& l, const float* A, i
 cudaError_t launch_amm_rt_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
                              int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done);
 bool amm_rt_applies(const TreesDev& t, const LutsDev& l, int es);
+// PQ encoder (mdn_pq.cu).
+cudaError_t launch_encode_pq(const TreesDev& t, const float* P_dense, const uint16_t* sub_b,
+                             const uint16_t* sub_e, const float* A, int64_t N, int64_t lda,
+                             uint8_t* codes, cudaStream_t s);
 // Column-major A (mdn_colmajor.cu).
 cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
                           int64_t ldt, float* out, int64_t ldo, cudaStream_t s);
@@ -108,13 +114,19 @@ struct mdn_model {
   std::vector<uint16_t> h_cols, h_slot;
   uint16_t* d_cols = nullptr;
   uint16_t* d_slot = nullptr;
+  bool pq = false;                // flags bit1: PQ comparator model, no trees
+  int pq_ds = 0;
+  std::vector<uint16_t> h_sub_e;  // [C] subspace end
+  uint16_t* d_sub_e = nullptr;
+  float* d_pqcent = nullptr;      // [16][DS/4][C][4]
   uint16_t* d_dims = nullptr;
   float* d_thr = nullptr;
   uint16_t* d_sub = nullptr;
   uint16_t* d_q = nullptr;
   float* d_P = nullptr;           // [16C][D]
   mdn::TreesDev trees() const {
-    return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8, q_byte, d_cols, d_slot, (int)h_cols.size()};
+    return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8, q_byte, d_cols, d_slot,
+            (int)h_cols.size(), d_pqcent, d_pqcent ? pq_ds : 0};
   }
 };
 

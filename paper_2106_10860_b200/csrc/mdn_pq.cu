@@ -1,0 +1,173 @@
+// Product Quantization encoder: the comparator MADDNESS replaces.
+//
+// g^(c)(a) = argmin_k sum_{j in J^(c)} (a_j - P^(c)_{k,j})^2  (PAPER.md Eq.
+// pqLoss, L182-184), K = 16 prototypes per subspace learned offline by
+// K-means (L155-163; oracle/pq.py). The codes use the same 4-bit packing as
+// mdn_encode and feed the same mdn_scan / tables (h(B) from the dense P).
+//
+// Floating point decides the integer code, so the distance is evaluated in the
+// order and precision the oracle uses (reading P1): fp32, every
+// subtract / multiply / add rounded separately (__fsub_rn / __fmul_rn /
+// __fadd_rn, no FMA contraction), j ascending; ties go to the lowest k.
+//
+// k_encode_pq<DS, R>: a thread owns one codebook c (lane % C) and R rows; the
+// 16 x DS prototypes of c are read from shared memory (layout [k][j/4][c][4]:
+// one conflict-free LDS.128 per 4 dims, reused for the R rows), so the kernel
+// is bound by the fp32 pipe: 3 * 16 * D flops per row (cls100: 24,576), not
+// by HBM -- which is the point of the comparison (Sec. 5.1).
+#include <cuda_runtime.h>
+
+#include "mdn_internal.h"
+#include "mdn_tma.cuh"
+
+namespace mdn {
+namespace fast {
+namespace pq {
+
+constexpr int THREADS = 256;
+
+template <int DS, int R>
+__global__ void __launch_bounds__(THREADS) k_encode_pq(const float* __restrict__ A, int64_t N,
+                                                       int64_t lda, int C,
+                                                       const float4* __restrict__ cent_g,
+                                                       uint8_t* __restrict__ codes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float4* s_cent = reinterpret_cast<float4*>(smem);             // [16][DS/4][C]
+  const int n4 = 16 * (DS / 4) * C;
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) s_cent[i] = cent_g[i];
+  __syncthreads();
+  const int c = threadIdx.x % C;
+  const int rg = threadIdx.x / C;
+  const int groups_per_block = THREADS / C;
+  const int64_t rows_per_block = (int64_t)groups_per_block * R;
+  // Block-uniform trip count (the code packing shuffles need every lane).
+  for (int64_t base = (int64_t)blockIdx.x * rows_per_block; base < N;
+       base += (int64_t)gridDim.x * rows_per_block) {
+    const int64_t row0 = base + (int64_t)rg * R;
+    float x[R][DS];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t row = row0 + r < N ? row0 + r : N - 1;     // clamp the tail (not stored)
+      const float4* src = reinterpret_cast<const float4*>(A + row * lda + (int64_t)c * DS);
+#pragma unroll
+      for (int j4 = 0; j4 < DS / 4; ++j4) {
+        const float4 v = __ldg(src + j4);
+        x[r][4 * j4] = v.x, x[r][4 * j4 + 1] = v.y, x[r][4 * j4 + 2] = v.z, x[r][4 * j4 + 3] = v.w;
+      }
+    }
+    float best[R];
+    uint32_t bk[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) best[r] = __int_as_float(0x7f800000), bk[r] = 0u;   // +inf
+#pragma unroll 1
+    for (int k = 0; k < 16; ++k) {
+      float d[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) d[r] = 0.f;
+#pragma unroll
+      for (int j4 = 0; j4 < DS / 4; ++j4) {
+        const float4 p = s_cent[(k * (DS / 4) + j4) * C + c];
+        const float pv[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const float t = __fsub_rn(x[r][4 * j4 + jj], pv[jj]);
+            d[r] = __fadd_rn(d[r], __fmul_rn(t, t));
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (d[r] < best[r]) best[r] = d[r], bk[r] = (uint32_t)k;   // strict: ties keep the lowest k
+    }
+    // pack two codes per byte: low nibble = even codebook (L147, L608)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t hi = __shfl_down_sync(0xffffffffu, bk[r], 1);
+      if ((c & 1) == 0 && row0 + r < N)
+        codes[(row0 + r) * (C / 2) + c / 2] = (uint8_t)(bk[r] | (hi << 4));
+    }
+  }
+}
+
+// Any subspace layout / C: thread per (row, codebook), prototypes from the
+// dense P in global memory.
+__global__ void k_encode_pq_generic(const float* __restrict__ A, int64_t N, int64_t lda, int C,
+                                    int D, const uint16_t* __restrict__ sub_b,
+                                    const uint16_t* __restrict__ sub_e,
+                                    const float* __restrict__ P, uint8_t* __restrict__ codes) {
+  const int nb = (C + 1) / 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N * nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / nb;
+    const int pair = (int)(i % nb);
+    uint32_t out = 0;
+    for (int h = 0; h < 2; ++h) {
+      const int c = 2 * pair + h;
+      if (c >= C) break;
+      float best = __int_as_float(0x7f800000);
+      uint32_t bk = 0;
+      for (int k = 0; k < 16; ++k) {
+        float d = 0.f;
+        for (int j = sub_b[c]; j < sub_e[c]; ++j) {
+          const float t = __fsub_rn(A[row * lda + j], P[(int64_t)(16 * c + k) * D + j]);
+          d = __fadd_rn(d, __fmul_rn(t, t));
+        }
+        if (d < best) best = d, bk = (uint32_t)k;
+      }
+      out |= bk << (4 * h);
+    }
+    codes[row * nb + pair] = (uint8_t)out;
+  }
+}
+
+template <int DS, int R>
+cudaError_t launch(const float* A, int64_t N, int64_t lda, int C, const float* cent,
+                   uint8_t* codes, cudaStream_t s) {
+  auto k = k_encode_pq<DS, R>;
+  const size_t smem = (size_t)16 * DS * C * 4;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t rows_per_block = (int64_t)(THREADS / C) * R;
+  int64_t blocks = (N + rows_per_block - 1) / rows_per_block;
+  const int64_t cap = (int64_t)dev_info().sms * per_sm;
+  if (blocks > cap) blocks = cap;
+  k<<<(unsigned)blocks, THREADS, smem, s>>>(A, N, lda, C, reinterpret_cast<const float4*>(cent),
+                                            codes);
+  return cudaGetLastError();
+}
+
+}  // namespace pq
+}  // namespace fast
+
+using namespace fast::pq;
+
+// t.pq_cent: [16][DS/4][C][4] prototypes when every subspace is [c DS, (c+1) DS)
+// with DS in {4, 8, 16, 32} and THREADS % C == 0 (else null: generic kernel).
+cudaError_t launch_encode_pq(const TreesDev& t, const float* P_dense, const uint16_t* sub_b,
+                             const uint16_t* sub_e, const float* A, int64_t N, int64_t lda,
+                             uint8_t* codes, cudaStream_t s) {
+  const bool fast_ok = t.pq_cent && t.pq_ds > 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
+                       lda % 4 == 0 && t.C % 2 == 0;
+  if (fast_ok) {
+    switch (t.pq_ds) {
+      case 4: return launch<4, 8>(A, N, lda, t.C, t.pq_cent, codes, s);
+      case 8: return launch<8, 8>(A, N, lda, t.C, t.pq_cent, codes, s);
+      case 16: return launch<16, 4>(A, N, lda, t.C, t.pq_cent, codes, s);
+      case 32: return launch<32, 2>(A, N, lda, t.C, t.pq_cent, codes, s);
+    }
+  }
+  const int64_t work = N * ((t.C + 1) / 2);
+  int64_t blocks = (work + 255) / 256;
+  const int64_t cap = (int64_t)fast::dev_info().sms * 8;
+  if (blocks > cap) blocks = cap;
+  k_encode_pq_generic<<<(unsigned)blocks, 256, 0, s>>>(A, N, lda, t.C, t.D, sub_b, sub_e, P_dense,
+                                                      codes);
+  return cudaGetLastError();
+}
+
+}  // namespace mdn
