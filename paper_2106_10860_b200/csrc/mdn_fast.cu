@@ -45,6 +45,14 @@ constexpr int NS_MAX = 8;                // A stage ring depth cap
 constexpr int BAR_BYTES = 256;
 constexpr int CM = -1;                   // SUBF value of the column-major-A variant
 
+// Shared-memory word offsets of codebook c's 16 thresholds / 4 split offsets.
+// The encoder lanes of a warp cover up to NG = C / 8 codebook groups (one
+// codebook 8g + i each at step i); padding by 8 (4) words per group puts the
+// groups' threshold (offset) blocks in different banks: conflict-free gathers
+// for NG <= 4, 2-way for NG = 8.
+__host__ __device__ constexpr int thr_base(int c) { return 16 * c + 8 * (c >> 3); }
+__host__ __device__ constexpr int off_base(int c) { return 4 * c + 4 * (c >> 3); }
+
 // Warp roles. Per row an encoder spends ~25 instructions per codebook
 // (4 split-dim loads, 4 threshold gathers, compares), a scanner ~4W per
 // codebook (W table words of 4 columns), so the encoder:scanner split follows
@@ -125,7 +133,7 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
 #pragma unroll
     for (int i = 0; i < G; ++i) {
       const int c = c0 + i;
-      const int4 o = *reinterpret_cast<const int4*>(s_off + 4 * c);
+      const int4 o = *reinterpret_cast<const int4*>(s_off + off_base(c));
       int x0, x1, x2, x3;
       if constexpr (SUBF <= 0) {
         x0 = rowp[o.x], x1 = rowp[o.y], x2 = rowp[o.z], x3 = rowp[o.w];
@@ -136,7 +144,7 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
         x0 = byte_of(wv[2 * i], wv[2 * i + 1], o.x), x1 = byte_of(wv[2 * i], wv[2 * i + 1], o.y);
         x2 = byte_of(wv[2 * i], wv[2 * i + 1], o.z), x3 = byte_of(wv[2 * i], wv[2 * i + 1], o.w);
       }
-      const int* th = s_q + 16 * c;
+      const int* th = s_q + thr_base(c);
       uint32_t p = x0 >= th[0] ? 1u : 0u;
       p = 2u * p + (x1 >= th[1 + p] ? 1u : 0u);
       p = 2u * p + (x2 >= th[3 + p] ? 1u : 0u);
@@ -148,7 +156,7 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
 #pragma unroll
   for (int i = 0; i < G; ++i) {
     const int c = c0 + i;
-    const int4 o = *reinterpret_cast<const int4*>(s_off + 4 * c);
+    const int4 o = *reinterpret_cast<const int4*>(s_off + off_base(c));
     float x0, x1, x2, x3;
     if constexpr (SUBF <= 0) {
       x0 = rowp[o.x], x1 = rowp[o.y], x2 = rowp[o.z], x3 = rowp[o.w];
@@ -165,7 +173,7 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
         x3 = (o.w & 4) ? pick4(v1, o.w) : pick4(v0, o.w);
       }
     }
-    const float* th = s_thr + 16 * c;
+    const float* th = s_thr + thr_base(c);
     // Algorithm 1: i <- 2i - 1 + [x_{j^t} >= v^t_i]  (0-based: p <- 2p + b)
     uint32_t p = x0 >= th[0] ? 1u : 0u;
     p = 2u * p + (x1 >= th[1 + p] ? 1u : 0u);
@@ -194,8 +202,8 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
   // Carve with integer offsets from `smem` so every pointer stays provably in
   // the shared window (plain LDS/STS, no generic loads).
   constexpr int OFF_THR = BAR_BYTES;
-  constexpr int OFF_OFF = OFF_THR + 16 * C * 4;
-  constexpr int OFF_BASE = OFF_OFF + 4 * C * 4;
+  constexpr int OFF_OFF = OFF_THR + thr_base(C) * 4;
+  constexpr int OFF_BASE = OFF_OFF + off_base(C) * 4;
   constexpr int OFF_COLS = OFF_BASE + C * 4;
   constexpr int OFF_LUT = (OFF_COLS + (SUBF == CM ? 4 * C * 4 : 0) + 15) & ~15;
   constexpr int OFF_CODES = OFF_LUT + (ENC_ONLY ? 0 : C * W * 16 * 4);
@@ -213,17 +221,19 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
 
   // ---- setup: trees, split-dim offsets, tables, barriers ----
   for (int i = tid; i < 16 * C; i += blockDim.x) {
+    const int si = thr_base(i / 16) + i % 16;
     if constexpr (sizeof(TIn) == 1)
-      reinterpret_cast<int*>(s_thr)[i] = p.q[i];   // integer split values (App. B, R11)
+      reinterpret_cast<int*>(s_thr)[si] = p.q[i];  // integer split values (App. B, R11)
     else
-      s_thr[i] = p.thr[i];
+      s_thr[si] = p.thr[i];
   }
   for (int i = tid; i < 4 * C; i += blockDim.x) {
     const int d = p.dims[i];
+    const int si = off_base(i / 4) + i % 4;
     if constexpr (SUBF == CM)
-      s_off[i] = p.slot[d] * p.slab_e;               // slot-major stage: [slot][row]
+      s_off[si] = p.slot[d] * p.slab_e;              // slot-major stage: [slot][row]
     else
-      s_off[i] = SUBF ? d - p.sub[i / 4] : (d / p.SW) * p.slab_e + (d % p.SW);
+      s_off[si] = SUBF ? d - p.sub[i / 4] : (d / p.SW) * p.slab_e + (d % p.SW);
   }
   if constexpr (SUBF == CM)
     for (int k = tid; k < p.nslab; k += blockDim.x) s_cols[k] = p.cols[k];
@@ -297,7 +307,11 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
         mbar_wait(&full[s], (q / p.NS) & 1u);
         const TIn* stg = s_stage + (size_t)s * stage_e;
         for (int u = etid; u < p.R * NG; u += EW * 32) {
-          const int r = u % p.R, g = u / p.R;
+          // Group-fastest units: the lanes of a warp cover NG codebook groups of
+          // 32 / NG rows, so their split columns differ and the per-row reads
+          // (pitch == 4 mod 32 words) spread over more banks than 32 rows of
+          // one column would (4-way conflicts: +47% shared wavefronts on scale).
+          const int g = NG > 1 ? u % NG : 0, r = NG > 1 ? u / NG : u;
           const uint32_t word = encode_group<TIn, C, SUBF>(stg + r * pitch, s_off, s_base, s_thr, g * G);
           const int row_local = st * p.R + r;
           if constexpr (ENC_ONLY) {
@@ -434,7 +448,7 @@ Geometry plan(int C, int W, int D, bool enc_only, int es) {
   g.SW = D / nslab;
   g.pad_e = pad_e;
   const int CBW = C >= 8 ? C / 8 : 1;
-  size_t fixed = BAR_BYTES + 16 * C * 4 + 4 * C * 4 + C * 4 + 16;
+  size_t fixed = BAR_BYTES + thr_base(C) * 4 + off_base(C) * 4 + C * 4 + 16;
   if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4;
   fixed = (fixed + 127) & ~size_t(127);
   const size_t budget = (size_t)dev_info().smem_optin;
@@ -686,7 +700,7 @@ static Geometry plan_cm(int C, int W, int n_cols, bool enc_only) {
   g.SW = 1;
   g.pad_e = 0;
   const int CBW = C >= 8 ? C / 8 : 1;
-  size_t fixed = BAR_BYTES + 16 * C * 4 + 4 * C * 4 + C * 4 + 4 * C * 4 + 16;
+  size_t fixed = BAR_BYTES + thr_base(C) * 4 + off_base(C) * 4 + C * 4 + 4 * C * 4 + 16;
   if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4;
   fixed = (fixed + 127) & ~size_t(127);
   const size_t budget = (size_t)dev_info().smem_optin;
