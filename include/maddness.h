@@ -84,6 +84,21 @@ void mdn_model_free(mdn_model* model);
 /* C, D and the file's FNV-1a fingerprint; any output pointer may be NULL. */
 int mdn_model_info(const mdn_model* model, int* C, int* D, uint64_t* fingerprint);
 
+/* GPU training: the offline step before the hot path (PAPER.md
+ * L379), Sec. 4.2-4.3 and App. C -- per codebook 4 x Algorithm 2 with
+ * Algorithms 3/4 (L252-305, L621-682), then ridge prototypes
+ * P = (G^T G + lambda I)^-1 G^T A~ (L318-321), or bucket means for lambda = 0
+ * (L218) -- with the readings R1-R12 of DESIGN.md.
+ *   A       device fp32 training rows A~, N x D, row stride lda >= D.
+ *   buf     host buffer receiving a "model.mdnm v1" stream (load it with
+ *           mdn_model_load); buf == NULL: *len receives the size needed,
+ *           48 + 76 C + 64 C D + 8 bytes. Otherwise *len is the capacity in,
+ *           bytes written out.
+ * Synchronous. Errors: MDN_EINVAL (bad sizes, a subspace wider than 64
+ * columns, lambda < 0), MDN_ENOMEM, MDN_ECUDA (incl. a failed Cholesky). */
+int mdn_train(const float* A, int64_t N, int64_t lda, int D, int C, double lambda, int device,
+              void* buf, size_t* len);
+
 /* ------------------------------------------------------------------ luts -- */
 
 /* h(B) + App. A quantisation (the "set_operator" step), computed on the device.

@@ -58,6 +58,7 @@ _SIGS = {
     "mdn_encode_cm": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "mdn_amm_cm": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "mdn_encode_pq": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
+    "mdn_train": (_i32, [_vp, _i64, _i64, _i32, _i32, ct.c_double, _i32, _vp, ct.POINTER(_sz)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -162,6 +163,19 @@ def mdn_model_load(buf: bytes, device: int = 0) -> Model:
     st = _lib.mdn_model_load(buf, len(buf), device, ct.byref(h), ct.byref(off))
     _check(st, "mdn_model_load", off.value if st == -3 else None)
     return Model(h, device)
+
+
+def mdn_train(A, C: int, lam: float = 1.0) -> bytes:
+    """GPU training (SURVEY N3): A is the CUDA fp32 training matrix A~ (N x D);
+    returns the "model.mdnm v1" bytes (load with mdn_model_load)."""
+    pa = _dev_ptr(A, "float32", "A")
+    n = _sz(0)
+    D = A.shape[1]
+    _check(_lib.mdn_train(None, 0, 0, D, C, lam, A.device.index or 0, None, ct.byref(n)), "mdn_train")
+    buf = ct.create_string_buffer(n.value)
+    _check(_lib.mdn_train(pa, A.shape[0], A.stride(0), D, C, lam, A.device.index or 0, buf,
+                          ct.byref(n)), "mdn_train")
+    return buf.raw[:n.value]
 
 
 def mdn_build_luts(model: Model, B, mode: int = MDN_SUM_EXACT, U: int = 16) -> Luts:

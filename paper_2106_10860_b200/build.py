@@ -60,7 +60,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if (force or not os.path.exists(LIB)
             or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)):
         tmp = LIB + ".tmp"
-        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcuda"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + [
+            "-lcuda", "-lcusolver", "-L/usr/local/cuda/lib64",
+            "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stdout}\n{p.stderr}")

@@ -280,6 +280,28 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   return MDN_OK;
 }
 
+int mdn_train(const float* A, int64_t N, int64_t lda, int D, int C, double lambda, int device,
+              void* buf, size_t* len) {
+  if (!len || C < 1 || D < 1 || C > D || C > MAX_C || D > 65535 || !(lambda >= 0)) return MDN_EINVAL;
+  const size_t need = train_blob_size(C, D);
+  if (!buf) {
+    *len = need;
+    return MDN_OK;
+  }
+  if (*len < need || !A || N < 1 || N > 0x7FFFFFFF || lda < D) return MDN_EINVAL;
+  DeviceGuard g(device);
+  if (!g.ok) return MDN_ECUDA;
+  std::vector<uint8_t> blob;
+  int err = MDN_OK;
+  cudaError_t e = train_model(A, N, lda, D, C, lambda, blob, &err);
+  if (e != cudaSuccess) return cuda_status(e);
+  if (err != MDN_OK) return err;
+  if (blob.size() != need) return MDN_ECUDA;
+  memcpy(buf, blob.data(), need);
+  *len = need;
+  return MDN_OK;
+}
+
 int mdn_model_info(const mdn_model* m, int* C, int* D, uint64_t* fp) {
   if (!m) return MDN_EINVAL;
   if (C) *C = m->C;

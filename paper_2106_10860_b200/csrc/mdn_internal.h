@@ -98,6 +98,11 @@ cudaError_t pack_words_dev(const uint8_t* dTq, int C, int M, uint32_t* dWords,
 
 uint64_t fnv1a64(const uint8_t* p, size_t n);
 
+// GPU training (mdn_train.cu): trees + prototypes -> model.mdnm v1.
+size_t train_blob_size(int C, int D);
+cudaError_t train_model(const float* A, int64_t N, int64_t lda, int D, int C, double lam,
+                        std::vector<uint8_t>& blob, int* err);
+
 }  // namespace mdn
 
 struct mdn_model {

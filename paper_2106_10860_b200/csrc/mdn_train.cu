@@ -1,0 +1,492 @@
+// GPU training of the MADDNESS hash trees and prototypes.
+//
+// The offline step before the hot path (untimed in the paper),
+// restated from Sec. 4.2-4.3 and App. C in the paper's order, with the same
+// readings as the oracle (R1-R12):
+//
+//   per codebook c (subspace J^(c), R1/R2), 4 times Algorithm 2 (L272-305):
+//     candidates  top-4 dims by L(j) = sum over buckets of the per-dim SSE
+//                 (L265; ties -> lower index, R3), evaluated ascending
+//     score       for each candidate j and bucket B: Algorithm 3 (L626-644)
+//                 on B sorted by x_j -- prefix / suffix SSE over all subspace
+//                 dims (Alg. 4, R4-R6), positions with x[n] < x[n+1] only
+//                 (R7, R9), first minimum (R8); keep j if the bucket-summed
+//                 loss is strictly smaller (L289)
+//     split       children {x_j < v}, {x_j >= v} (L296-302, L240), order kept
+//   prototypes    ridge P = (G^T G + lambda I)^-1 G^T A~ (L318-321) with G
+//                 from the leaves (R12), or bucket means for lambda = 0 (L218)
+//
+// Device layout: the rows of each bucket are a contiguous range of `perm`
+// (ascending row id inside a bucket, as the oracle's index arrays). Sorting a
+// bucket by x_j is a CUB segmented stable sort (a library primitive); the
+// prefix sums, losses, argmins and partitions are the kernels below; the SPD
+// solve is cuSOLVER's Cholesky (potrf / potrs).
+//
+// Precision: fp64 statistics as the oracle; the loss of a position sums the
+// subspace dims in ascending order. Block-parallel prefix sums add in a
+// different order than the oracle's sequential cumsum, so on fp32 data a split
+// whose loss ties another within rounding may differ (both are optimal to
+// rounding); on integer-valued data (8-bit pixels) every sum is exact and the
+// trees are bit-identical (tests/test_gpu_train.py).
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "mdn_internal.h"
+
+namespace mdn {
+namespace train {
+
+constexpr int TB = 256;   // threads per block of the per-bucket kernels
+
+// L(j, B) for every subspace dim of every bucket (two-pass: mean, then squared
+// deviations; L259). out[b * d + jj].
+__global__ void k_dim_sse(const float* __restrict__ A, int64_t lda, const int* __restrict__ perm,
+                          const int* __restrict__ bstart, int col0, int d, double* __restrict__ out) {
+  using BR = cub::BlockReduce<double, TB>;
+  __shared__ typename BR::TempStorage tmp;
+  __shared__ double s_mean;
+  const int b = blockIdx.x, jj = blockIdx.y;
+  const int s = bstart[b], e = bstart[b + 1], n = e - s;
+  if (n == 0) {
+    if (threadIdx.x == 0) out[b * d + jj] = 0.0;
+    return;
+  }
+  double acc = 0.0;
+  for (int i = s + threadIdx.x; i < e; i += TB) acc += (double)A[(int64_t)perm[i] * lda + col0 + jj];
+  double tot = BR(tmp).Sum(acc);
+  if (threadIdx.x == 0) s_mean = tot / n;
+  __syncthreads();
+  const double mean = s_mean;
+  acc = 0.0;
+  for (int i = s + threadIdx.x; i < e; i += TB) {
+    const double t = (double)A[(int64_t)perm[i] * lda + col0 + jj] - mean;
+    acc += t * t;
+  }
+  tot = BR(tmp).Sum(acc);
+  if (threadIdx.x == 0) out[b * d + jj] = tot;
+}
+
+// Sort keys for a candidate column: x_j of the rows in perm order (-0 -> +0).
+__global__ void k_gather_keys(const float* __restrict__ A, int64_t lda, const int* __restrict__ perm,
+                              int N, int col, float* __restrict__ keys, int* __restrict__ vals) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const int r = perm[i];
+    keys[i] = A[(int64_t)r * lda + col] + 0.0f;
+    vals[i] = r;
+  }
+}
+
+__device__ __forceinline__ float midpoint_threshold(float a, float b) {
+  // Alg. 3 line 9 (L639) with reading R9: a < v <= b in fp32.
+  float v = __double2float_rn(__dadd_rn((double)a, __ddiv_rn(__dsub_rn((double)b, (double)a), 2.0)));
+  if (v <= a) v = nextafterf(a, INFINITY);
+  return v;
+}
+
+// Algorithm 3 on every bucket for one candidate column. Rows of bucket b are
+// keys/vals[bstart[b] .. bstart[b+1]) sorted by x_j. Outputs per bucket the
+// loss of the best realisable split and its threshold.
+template <int DMAX>
+__global__ void __launch_bounds__(TB) k_split_loss(const float* __restrict__ A, int64_t lda,
+                                                   const float* __restrict__ keys,
+                                                   const int* __restrict__ vals,
+                                                   const int* __restrict__ bstart, int col0, int d,
+                                                   double* __restrict__ loss_out,
+                                                   float* __restrict__ thr_out) {
+  using BS = cub::BlockScan<double, TB>;
+  using BR = cub::BlockReduce<double, TB>;
+  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ typename BR::TempStorage red_tmp;
+  __shared__ double s_T1[DMAX], s_T2[DMAX], s_c1[DMAX], s_c2[DMAX];
+  __shared__ double s_bl[TB];
+  __shared__ int s_bn[TB];
+  const int b = blockIdx.x;
+  const int s = bstart[b], e = bstart[b + 1], N = e - s;
+  if (N == 0) {                                            // R10
+    if (threadIdx.x == 0) loss_out[b] = 0.0, thr_out[b] = 0.f;
+    return;
+  }
+  // bucket totals per dim (for the suffix sums: tail = total - prefix)
+  for (int jj = 0; jj < d; ++jj) {
+    double a1 = 0.0, a2 = 0.0;
+    for (int i = s + threadIdx.x; i < e; i += TB) {
+      const double x = (double)A[(int64_t)vals[i] * lda + col0 + jj];
+      a1 += x, a2 += x * x;
+    }
+    const double t1 = BR(red_tmp).Sum(a1);
+    __syncthreads();
+    const double t2 = BR(red_tmp).Sum(a2);
+    if (threadIdx.x == 0) s_T1[jj] = t1, s_T2[jj] = t2, s_c1[jj] = 0.0, s_c2[jj] = 0.0;
+    __syncthreads();
+  }
+  double best = INFINITY;
+  int best_n = -1;
+  for (int base = 0; base < N; base += TB) {
+    const int n = base + threadIdx.x;                       // position in the bucket (0-based)
+    const bool in = n < N;
+    const bool valid = n + 1 < N && keys[s + n] < keys[s + n + 1];   // R7 + R9
+    const int row = in ? vals[s + n] : 0;
+    double head = 0.0, tail = 0.0;
+    for (int jj = 0; jj < d; ++jj) {
+      const double x = in ? (double)A[(int64_t)row * lda + col0 + jj] : 0.0;
+      double p1, p2, agg1, agg2;
+      BS(scan_tmp).InclusiveSum(x, p1, agg1);
+      __syncthreads();
+      BS(scan_tmp).InclusiveSum(x * x, p2, agg2);
+      __syncthreads();
+      p1 += s_c1[jj], p2 += s_c2[jj];                       // carry from earlier tiles
+      const double cnt = (double)(n + 1), rest = (double)(N - n - 1);
+      head += p2 - p1 * p1 / cnt;                           // Alg. 4, dims ascending
+      if (rest > 1) {                                       // rest == 1: L662's out[0] = 0
+        const double r1 = s_T1[jj] - p1, r2 = s_T2[jj] - p2;
+        tail += r2 - r1 * r1 / rest;
+      }
+      __syncthreads();
+      if (threadIdx.x == TB - 1) s_c1[jj] += agg1, s_c2[jj] += agg2;
+      __syncthreads();
+    }
+    if (n == 0) head = 0.0;                                 // L662: out[0] = 0
+    if (valid) {
+      const double l = head + tail;                         // L634-635
+      if (l < best) best = l, best_n = n;                   // ascending n: first minimum
+    }
+  }
+  s_bl[threadIdx.x] = best;
+  s_bn[threadIdx.x] = best_n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bl = INFINITY;
+    int bn = -1;
+    for (int t = 0; t < TB; ++t)                            // lowest position on ties (R8)
+      if (s_bn[t] >= 0 && (s_bl[t] < bl || (s_bl[t] == bl && s_bn[t] < bn))) bl = s_bl[t], bn = s_bn[t];
+    if (bn < 0) {
+      // constant column: (the value, SSE of the bucket), every row goes right
+      double sse = 0.0;
+      for (int jj = 0; jj < d; ++jj) sse += s_T2[jj] - s_T1[jj] * s_T1[jj] / (double)N;
+      loss_out[b] = sse;
+      thr_out[b] = keys[s];
+    } else {
+      loss_out[b] = bl;
+      thr_out[b] = midpoint_threshold(keys[s + bn], keys[s + bn + 1]);
+    }
+  }
+}
+
+// Stable partition of each bucket by x_j >= v_b (L296-302): left child 2b,
+// right child 2b+1, ascending row id kept inside each.
+__global__ void k_partition(const float* __restrict__ A, int64_t lda, const int* __restrict__ perm,
+                            const int* __restrict__ bstart, int col, const float* __restrict__ thr,
+                            int* __restrict__ perm_out, int* __restrict__ nleft_out) {
+  using BS = cub::BlockScan<int, TB>;
+  using BR = cub::BlockReduce<int, TB>;
+  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ typename BR::TempStorage red_tmp;
+  __shared__ int s_left, s_carry_l, s_carry_r;
+  const int b = blockIdx.x;
+  const int s = bstart[b], e = bstart[b + 1];
+  const float v = thr[b];
+  int cl = 0;
+  for (int i = s + threadIdx.x; i < e; i += TB) cl += (A[(int64_t)perm[i] * lda + col] < v) ? 1 : 0;
+  const int nl = BR(red_tmp).Sum(cl);
+  if (threadIdx.x == 0) s_left = nl, s_carry_l = 0, s_carry_r = 0, nleft_out[b] = nl;
+  __syncthreads();
+  const int left_total = s_left;
+  for (int base = s; base < e; base += TB) {
+    const int i = base + threadIdx.x;
+    const bool in = i < e;
+    const int r = in ? perm[i] : 0;
+    const int isl = in && A[(int64_t)r * lda + col] < v ? 1 : 0;
+    const int isr = in && !isl ? 1 : 0;
+    int pl, pr, al, ar;
+    BS(scan_tmp).ExclusiveSum(isl, pl, al);
+    __syncthreads();
+    BS(scan_tmp).ExclusiveSum(isr, pr, ar);
+    if (isl) perm_out[s + s_carry_l + pl] = r;
+    if (isr) perm_out[s + left_total + s_carry_r + pr] = r;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry_l += al, s_carry_r += ar;
+    __syncthreads();
+  }
+}
+
+// codes[row * C + c] = leaf of row for codebook c.
+__global__ void k_leaf_codes(const int* __restrict__ perm, const int* __restrict__ bstart, int c,
+                             int C, uint8_t* __restrict__ codes) {
+  const int b = blockIdx.x;
+  for (int i = bstart[b] + threadIdx.x; i < bstart[b + 1]; i += blockDim.x)
+    codes[(int64_t)perm[i] * C + c] = (uint8_t)b;
+}
+
+// G^T G co-occurrence counts (L318): M[(c,k),(c',k')] += 1 per row.
+__global__ void k_gtg(const uint8_t* __restrict__ codes, int N, int C, unsigned* __restrict__ M) {
+  const int KC = 16 * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)N * C * C;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i / ((int64_t)C * C));
+    const int cc = (int)(i % ((int64_t)C * C));
+    const int c1 = cc / C, c2 = cc % C;
+    const int a = 16 * c1 + codes[(int64_t)row * C + c1], bb = 16 * c2 + codes[(int64_t)row * C + c2];
+    atomicAdd(&M[(int64_t)a * KC + bb], 1u);
+  }
+}
+
+// G^T A~ for one leaf (c, k): sum of its rows over every column j (leaf rows
+// are the contiguous perm range of the final level). Column-major for potrs:
+// out[j * KC + 16c + k]. With bucket means (lambda = 0) the mean is taken
+// over the subspace only and written row-major into P directly.
+__global__ void k_gta(const float* __restrict__ A, int64_t lda, int D, const int* __restrict__ perm,
+                      const int* __restrict__ bstart, int c, int KC, double* __restrict__ GtA) {
+  using BR = cub::BlockReduce<double, TB>;
+  __shared__ typename BR::TempStorage tmp;
+  const int k = blockIdx.x;
+  const int s = bstart[k], e = bstart[k + 1];
+  for (int j = blockIdx.y; j < D; j += gridDim.y) {
+    double acc = 0.0;
+    for (int i = s + threadIdx.x; i < e; i += TB) acc += (double)A[(int64_t)perm[i] * lda + j];
+    const double tot = BR(tmp).Sum(acc);
+    if (threadIdx.x == 0) GtA[(int64_t)j * KC + 16 * c + k] = tot;
+    __syncthreads();
+  }
+}
+
+__global__ void k_add_ridge(const unsigned* __restrict__ cnt, double* __restrict__ M, int KC,
+                            double lam) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)KC * KC;
+       i += (int64_t)gridDim.x * blockDim.x)
+    M[i] = (double)cnt[i] + ((i / KC) == (i % KC) ? lam : 0.0);
+}
+
+}  // namespace train
+
+using namespace train;
+
+namespace {
+
+struct DevBuf {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, (n ? n : 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~DevBuf() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+template <class T>
+void put(std::vector<uint8_t>& o, T v) {
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+  o.insert(o.end(), b, b + sizeof(T));
+}
+
+}  // namespace
+
+size_t train_blob_size(int C, int D) { return 48 + (size_t)76 * C + (size_t)64 * C * D + 8; }
+
+// Trains on device rows A (N x D, lda) and serialises "model.mdnm v1" into
+// `blob`. Returns a cudaError_t; *err = MDN_* for non-CUDA failures.
+cudaError_t train_model(const float* A, int64_t N64, int64_t lda, int D, int C, double lam,
+                        std::vector<uint8_t>& blob, int* err) {
+  *err = MDN_OK;
+  const int N = (int)N64;
+  const int KC = 16 * C;
+  // R1: contiguous subspaces, the first D mod C one column wider.
+  std::vector<int> sb(C), se(C);
+  {
+    const int base = D / C, extra = D % C;
+    int b = 0;
+    for (int c = 0; c < C; ++c) {
+      sb[c] = b;
+      b += base + (c < extra ? 1 : 0);
+      se[c] = b;
+    }
+  }
+  int dmax = 0;
+  for (int c = 0; c < C; ++c) dmax = std::max(dmax, se[c] - sb[c]);
+  if (dmax > 64) {
+    *err = MDN_EINVAL;     // the split-loss kernel keeps <= 64 per-dim totals in shared memory
+    return cudaSuccess;
+  }
+  DevBuf buf;
+  int* perm = buf.get<int>(N);
+  int* perm2 = buf.get<int>(N);
+  int* vals = buf.get<int>(N);
+  int* vals_s = buf.get<int>(N);
+  float* keys = buf.get<float>(N);
+  float* keys_s = buf.get<float>(N);
+  int* d_bstart = buf.get<int>(17);
+  int* d_nleft = buf.get<int>(16);
+  double* d_L = buf.get<double>(16 * 64);
+  double* d_loss = buf.get<double>(16);
+  float* d_thr = buf.get<float>(16);
+  uint8_t* d_codes = buf.get<uint8_t>((size_t)N * C);
+  unsigned* d_cnt = buf.get<unsigned>((size_t)KC * KC);
+  double* d_M = buf.get<double>((size_t)KC * KC);
+  double* d_GtA = buf.get<double>((size_t)KC * D);
+  if (!perm || !perm2 || !vals || !vals_s || !keys || !keys_s || !d_bstart || !d_nleft || !d_L ||
+      !d_loss || !d_thr || !d_codes || !d_cnt || !d_M || !d_GtA) {
+    *err = MDN_ENOMEM;
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMemset(d_GtA, 0, (size_t)KC * D * sizeof(double));
+  if (e != cudaSuccess) return e;
+  std::vector<int> h_perm(N);
+  for (int i = 0; i < N; ++i) h_perm[i] = i;
+  // CUB temp storage (sized for the largest call: N items, 8 segments)
+  size_t cub_bytes = 0;
+  for (int nseg : {1, 2, 4, 8}) {
+    size_t b = 0;
+    cub::DeviceSegmentedSort::StableSortPairs(nullptr, b, keys, keys_s, vals, vals_s, N, nseg,
+                                              d_bstart, d_bstart + 1);
+    cub_bytes = std::max(cub_bytes, b);
+  }
+  void* cub_tmp = buf.get<uint8_t>(cub_bytes);
+  if (!cub_tmp) {
+    *err = MDN_ENOMEM;
+    return cudaSuccess;
+  }
+  std::vector<uint16_t> dims((size_t)C * 4);
+  std::vector<float> thr((size_t)C * 15, 0.f);
+  const int gk_blocks = std::min(4096, (N + 255) / 256);
+  for (int c = 0; c < C; ++c) {
+    const int col0 = sb[c], d = se[c] - sb[c];
+    if ((e = cudaMemcpy(perm, h_perm.data(), (size_t)N * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    std::vector<int> bst = {0, N};
+    for (int t = 0; t < 4; ++t) {
+      const int nb = 1 << t;
+      if ((e = cudaMemcpy(d_bstart, bst.data(), (nb + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+      // candidates (L265): top-4 of L(j) summed over buckets in bucket order
+      k_dim_sse<<<dim3(nb, d), TB>>>(A, lda, perm, d_bstart, col0, d, d_L);
+      std::vector<double> hL((size_t)nb * d);
+      if ((e = cudaMemcpy(hL.data(), d_L, hL.size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+      std::vector<double> L(d, 0.0);
+      for (int b = 0; b < nb; ++b)
+        for (int jj = 0; jj < d; ++jj) L[jj] += hL[(size_t)b * d + jj];
+      std::vector<int> order(d);
+      for (int jj = 0; jj < d; ++jj) order[jj] = jj;
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return L[x] > L[y]; });
+      std::vector<int> cand(order.begin(), order.begin() + std::min(4, d));
+      std::sort(cand.begin(), cand.end());
+      // score each candidate (Alg. 2 l.4-15)
+      double l_min = INFINITY;
+      int j_min = -1;
+      std::vector<float> v_min(nb);
+      for (int jj : cand) {
+        k_gather_keys<<<gk_blocks, 256>>>(A, lda, perm, N, col0 + jj, keys, vals);
+        size_t bytes = cub_bytes;
+        e = cub::DeviceSegmentedSort::StableSortPairs(cub_tmp, bytes, keys, keys_s, vals, vals_s, N, nb,
+                                                      d_bstart, d_bstart + 1);
+        if (e != cudaSuccess) return e;
+        if (dmax <= 16)
+          k_split_loss<16><<<nb, TB>>>(A, lda, keys_s, vals_s, d_bstart, col0, d, d_loss, d_thr);
+        else
+          k_split_loss<64><<<nb, TB>>>(A, lda, keys_s, vals_s, d_bstart, col0, d, d_loss, d_thr);
+        std::vector<double> hl(nb);
+        std::vector<float> hv(nb);
+        if ((e = cudaMemcpy(hl.data(), d_loss, nb * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+        if ((e = cudaMemcpy(hv.data(), d_thr, nb * 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+        double l = 0.0;
+        for (int b = 0; b < nb; ++b) l += hl[b];              // L287, bucket order
+        if (l < l_min) l_min = l, j_min = jj, v_min = hv;     // L289 (strict)
+      }
+      dims[(size_t)c * 4 + t] = (uint16_t)(col0 + j_min);
+      for (int b = 0; b < nb; ++b) thr[(size_t)c * 15 + (1 << t) - 1 + b] = v_min[b];
+      // split (L296-302)
+      if ((e = cudaMemcpy(d_thr, v_min.data(), nb * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+      k_partition<<<nb, TB>>>(A, lda, perm, d_bstart, col0 + j_min, d_thr, perm2, d_nleft);
+      std::vector<int> nl(nb);
+      if ((e = cudaMemcpy(nl.data(), d_nleft, nb * 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+      std::vector<int> nbst(2 * nb + 1);
+      for (int b = 0; b < nb; ++b) nbst[2 * b] = bst[b], nbst[2 * b + 1] = bst[b] + nl[b];
+      nbst[2 * nb] = N;
+      bst = nbst;
+      std::swap(perm, perm2);
+    }
+    // leaves -> codes (R12: membership == re-encoding under R9) and G^T A~
+    if ((e = cudaMemcpy(d_bstart, bst.data(), 17 * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    k_leaf_codes<<<16, 256>>>(perm, d_bstart, c, C, d_codes);
+    k_gta<<<dim3(16, std::min(D, 1024)), TB>>>(A, lda, D, perm, d_bstart, c, KC, d_GtA);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  // prototypes
+  std::vector<float> P((size_t)KC * D, 0.f);
+  std::vector<double> X((size_t)KC * D);
+  if (lam > 0) {
+    if ((e = cudaMemset(d_cnt, 0, (size_t)KC * KC * 4)) != cudaSuccess) return e;
+    k_gtg<<<4096, 256>>>(d_codes, N, C, d_cnt);
+    k_add_ridge<<<1024, 256>>>(d_cnt, d_M, KC, lam);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    cusolverDnHandle_t h = nullptr;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) {
+      *err = MDN_ECUDA;
+      return cudaSuccess;
+    }
+    int lwork = 0;
+    int* d_info = buf.get<int>(1);
+    cusolverStatus_t cs = cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, KC, d_M, KC, &lwork);
+    double* work = buf.get<double>((size_t)std::max(lwork, 1));
+    if (cs == CUSOLVER_STATUS_SUCCESS)
+      cs = cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, KC, d_M, KC, work, lwork, d_info);
+    if (cs == CUSOLVER_STATUS_SUCCESS)
+      cs = cusolverDnDpotrs(h, CUBLAS_FILL_MODE_LOWER, KC, D, d_M, KC, d_GtA, KC, d_info);
+    cusolverDnDestroy(h);
+    int info = 0;
+    if ((e = cudaMemcpy(&info, d_info, 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+    if (cs != CUSOLVER_STATUS_SUCCESS || info != 0) {
+      *err = MDN_ECUDA;
+      return cudaSuccess;
+    }
+    if ((e = cudaMemcpy(X.data(), d_GtA, X.size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+    for (int ck = 0; ck < KC; ++ck)
+      for (int j = 0; j < D; ++j) P[(size_t)ck * D + j] = (float)X[(size_t)j * KC + ck];
+  } else {
+    // bucket means over the subspace (L218, MADDNESS-PQ), zero for empty leaves (R10)
+    std::vector<uint8_t> hc((size_t)N * C);
+    if ((e = cudaMemcpy(X.data(), d_GtA, X.size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(hc.data(), d_codes, hc.size(), cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+    std::vector<int64_t> cnt((size_t)KC, 0);
+    for (int n = 0; n < N; ++n)
+      for (int c = 0; c < C; ++c) cnt[16 * c + hc[(size_t)n * C + c]]++;
+    for (int c = 0; c < C; ++c)
+      for (int k = 0; k < 16; ++k) {
+        const int ck = 16 * c + k;
+        if (!cnt[ck]) continue;
+        for (int j = sb[c]; j < se[c]; ++j) P[(size_t)ck * D + j] = (float)(X[(size_t)j * KC + ck] / cnt[ck]);
+      }
+  }
+  // serialise model.mdnm v1 (include/maddness.h)
+  blob.clear();
+  blob.insert(blob.end(), {'M', 'D', 'N', 'M'});
+  put<uint32_t>(blob, 1);
+  put<uint32_t>(blob, (uint32_t)C);
+  put<uint32_t>(blob, (uint32_t)D);
+  put<uint32_t>(blob, 16);
+  put<uint32_t>(blob, lam > 0 ? 1u : 0u);
+  put<double>(blob, lam);
+  put<uint64_t>(blob, (uint64_t)N);
+  put<uint64_t>(blob, 0);
+  for (int c = 0; c < C; ++c) {
+    put<uint32_t>(blob, (uint32_t)sb[c]);
+    put<uint32_t>(blob, (uint32_t)se[c]);
+    for (int t = 0; t < 4; ++t) put<uint16_t>(blob, dims[(size_t)c * 4 + t]);
+    for (int i = 0; i < 15; ++i) put<float>(blob, thr[(size_t)c * 15 + i]);
+  }
+  const uint8_t* pb = reinterpret_cast<const uint8_t*>(P.data());
+  blob.insert(blob.end(), pb, pb + P.size() * 4);
+  put<uint64_t>(blob, fnv1a64(blob.data(), blob.size()));
+  return cudaSuccess;
+}
+
+}  // namespace mdn
