@@ -225,6 +225,58 @@ def run_reference(args):
     return 0
 
 
+def run_train(args):
+    """--op train: mdn_train on the config's training split, timed
+    per full training (trees + ridge prototypes); the oracle's training timed
+    beside it on a bounded sample (its per-codebook tree learning, scaled)."""
+    import torch
+    import paper_2106_10860_b200 as mdn
+    from datagen.synth import CONFIGS, make_config_data
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    name = args.config
+    spec = CONFIGS[name]
+    A_h = make_config_data(name, n_test=0)[0].astype(np.float32)
+    A = torch.from_numpy(A_h).cuda()
+    for _ in range(args.warmup):
+        blob = mdn.mdn_train(A, spec.C, 1.0)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        blob = mdn.mdn_train(A, spec.C, 1.0)                 # synchronous
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        sub = O.subspaces(spec.D, spec.C)
+        t_tree, k = 0.0, 0
+        while k < spec.C and (t_tree < args.cpu_seconds or k == 0):
+            b0, e0 = sub[k]
+            s0 = time.perf_counter()
+            O.learn_hash_tree(A_h[:, b0:e0])
+            t_tree += time.perf_counter() - s0
+            k += 1
+        est = t_tree / k * spec.C
+        cpu = {"value": A_h.shape[0] / est, "unit": "rows/s", "cores": 1, "kind": "oracle",
+               "sample": f"oracle tree learning (Alg. 2-4) of {k} of {spec.C} codebooks "
+                         f"({t_tree:.1f} s), scaled to all codebooks; ridge excluded"}
+    line = {"metric": f"MADDNESS training rows/s ({name}: N={A_h.shape[0]}, D={spec.D}, C={spec.C}) "
+                      "[train only]",
+            "value": A_h.shape[0] / t, "unit": "rows/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{name} training split, trees + ridge prototypes (lambda = 1)",
+                       "rows": int(A_h.shape[0])},
+            "roofline": None, "cpu_baseline": cpu, "e2e": None, "gpu_launches": None,
+            "op": "train", "model_bytes": len(blob),
+            "note": "offline step, untimed in the paper (L379); wall time of the synchronous call"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run(args):
     import torch
     import torch.distributed as dist
@@ -519,8 +571,9 @@ def main():
     ap.add_argument("--config", default=CONFIG,
                     help="workload (default: the headline cls100 config); others for DESIGN.md tables")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--op", choices=["amm", "encode", "scan"], default="amm",
-                    help="amm (the hot path, default) or the unfused halves, for DESIGN.md")
+    ap.add_argument("--op", choices=["amm", "encode", "scan", "train"], default="amm",
+                    help="amm (the hot path, default), the unfused halves, or train: GPU "
+                         "training (SURVEY N3) on the config's training split, for DESIGN.md")
     ap.add_argument("--encoder", choices=["maddness", "pq"], default="maddness",
                     help="maddness (the method) or pq: the PQ comparator encoder (SURVEY N4) "
                          "feeding the same scan")
@@ -531,6 +584,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.op == "train":
+        return run_train(args)
     return run(args)
 
 

@@ -36,6 +36,7 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -46,42 +47,57 @@ namespace mdn {
 namespace train {
 
 constexpr int TB = 256;   // threads per block of the per-bucket kernels
+constexpr int BS = 17;    // bucket-offset stride per codebook (<= 16 buckets + 1)
+
+// All codebooks are trained together: blockIdx.{y,z} selects the codebook c,
+// whose rows sit in perm[c N ..), buckets at bstart[c BS ..), subspace at
+// col0[c] with d[c] dims.
 
 // L(j, B) for every subspace dim of every bucket (two-pass: mean, then squared
-// deviations; L259). out[b * d + jj].
+// deviations; L259). grid (nb, dmax, C); out[(c 16 + b) 64 + jj].
 __global__ void k_dim_sse(const float* __restrict__ A, int64_t lda, const int* __restrict__ perm,
-                          const int* __restrict__ bstart, int col0, int d, double* __restrict__ out) {
+                          const int* __restrict__ bstart, const int* __restrict__ col0,
+                          const int* __restrict__ dims_n, int N, double* __restrict__ out) {
   using BR = cub::BlockReduce<double, TB>;
   __shared__ typename BR::TempStorage tmp;
   __shared__ double s_mean;
-  const int b = blockIdx.x, jj = blockIdx.y;
-  const int s = bstart[b], e = bstart[b + 1], n = e - s;
+  const int b = blockIdx.x, jj = blockIdx.y, c = blockIdx.z;
+  if (jj >= dims_n[c]) return;
+  const int* pc = perm + (size_t)c * N;
+  const int s = bstart[c * BS + b], e = bstart[c * BS + b + 1], n = e - s;
+  const int col = col0[c] + jj;
+  double* o = out + ((size_t)c * 16 + b) * 64 + jj;
   if (n == 0) {
-    if (threadIdx.x == 0) out[b * d + jj] = 0.0;
+    if (threadIdx.x == 0) *o = 0.0;
     return;
   }
   double acc = 0.0;
-  for (int i = s + threadIdx.x; i < e; i += TB) acc += (double)A[(int64_t)perm[i] * lda + col0 + jj];
+  for (int i = s + threadIdx.x; i < e; i += TB) acc += (double)A[(int64_t)pc[i] * lda + col];
   double tot = BR(tmp).Sum(acc);
   if (threadIdx.x == 0) s_mean = tot / n;
   __syncthreads();
   const double mean = s_mean;
   acc = 0.0;
   for (int i = s + threadIdx.x; i < e; i += TB) {
-    const double t = (double)A[(int64_t)perm[i] * lda + col0 + jj] - mean;
+    const double t = (double)A[(int64_t)pc[i] * lda + col] - mean;
     acc += t * t;
   }
   tot = BR(tmp).Sum(acc);
-  if (threadIdx.x == 0) out[b * d + jj] = tot;
+  if (threadIdx.x == 0) *o = tot;
 }
 
-// Sort keys for a candidate column: x_j of the rows in perm order (-0 -> +0).
+// Sort keys for each codebook's candidate column: x_j of the rows in perm
+// order (-0 -> +0). grid (x, C).
 __global__ void k_gather_keys(const float* __restrict__ A, int64_t lda, const int* __restrict__ perm,
-                              int N, int col, float* __restrict__ keys, int* __restrict__ vals) {
+                              int N, const int* __restrict__ cols, float* __restrict__ keys,
+                              int* __restrict__ vals) {
+  const int c = blockIdx.y;
+  const int col = cols[c];
+  const size_t off = (size_t)c * N;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-    const int r = perm[i];
-    keys[i] = A[(int64_t)r * lda + col] + 0.0f;
-    vals[i] = r;
+    const int r = perm[off + i];
+    keys[off + i] = A[(int64_t)r * lda + col] + 0.0f;
+    vals[off + i] = r;
   }
 }
 
@@ -92,27 +108,34 @@ __device__ __forceinline__ float midpoint_threshold(float a, float b) {
   return v;
 }
 
-// Algorithm 3 on every bucket for one candidate column. Rows of bucket b are
-// keys/vals[bstart[b] .. bstart[b+1]) sorted by x_j. Outputs per bucket the
-// loss of the best realisable split and its threshold.
+// Algorithm 3 on every bucket of every codebook for one candidate column each.
+// Rows of bucket b of codebook c are keys/vals[c N + bstart[c BS + b] ..) sorted
+// by x_j. grid (nb, C); outputs per (c, b) the loss of the best realisable
+// split and its threshold.
 template <int DMAX>
 __global__ void __launch_bounds__(TB) k_split_loss(const float* __restrict__ A, int64_t lda,
-                                                   const float* __restrict__ keys,
-                                                   const int* __restrict__ vals,
-                                                   const int* __restrict__ bstart, int col0, int d,
+                                                   const float* __restrict__ keys_all,
+                                                   const int* __restrict__ vals_all,
+                                                   const int* __restrict__ bstart,
+                                                   const int* __restrict__ col0_a,
+                                                   const int* __restrict__ dims_n, int Nrows,
                                                    double* __restrict__ loss_out,
                                                    float* __restrict__ thr_out) {
-  using BS = cub::BlockScan<double, TB>;
+  using BSc = cub::BlockScan<double, TB>;
   using BR = cub::BlockReduce<double, TB>;
-  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ typename BSc::TempStorage scan_tmp;
   __shared__ typename BR::TempStorage red_tmp;
   __shared__ double s_T1[DMAX], s_T2[DMAX], s_c1[DMAX], s_c2[DMAX];
   __shared__ double s_bl[TB];
   __shared__ int s_bn[TB];
-  const int b = blockIdx.x;
-  const int s = bstart[b], e = bstart[b + 1], N = e - s;
+  const int b = blockIdx.x, c = blockIdx.y;
+  const float* keys = keys_all + (size_t)c * Nrows;
+  const int* vals = vals_all + (size_t)c * Nrows;
+  const int col0 = col0_a[c], d = dims_n[c];
+  const int s = bstart[c * BS + b], e = bstart[c * BS + b + 1], N = e - s;
+  const int ob = c * 16 + b;
   if (N == 0) {                                            // R10
-    if (threadIdx.x == 0) loss_out[b] = 0.0, thr_out[b] = 0.f;
+    if (threadIdx.x == 0) loss_out[ob] = 0.0, thr_out[ob] = 0.f;
     return;
   }
   // bucket totals per dim (for the suffix sums: tail = total - prefix)
@@ -139,9 +162,9 @@ __global__ void __launch_bounds__(TB) k_split_loss(const float* __restrict__ A, 
     for (int jj = 0; jj < d; ++jj) {
       const double x = in ? (double)A[(int64_t)row * lda + col0 + jj] : 0.0;
       double p1, p2, agg1, agg2;
-      BS(scan_tmp).InclusiveSum(x, p1, agg1);
+      BSc(scan_tmp).InclusiveSum(x, p1, agg1);
       __syncthreads();
-      BS(scan_tmp).InclusiveSum(x * x, p2, agg2);
+      BSc(scan_tmp).InclusiveSum(x * x, p2, agg2);
       __syncthreads();
       p1 += s_c1[jj], p2 += s_c2[jj];                       // carry from earlier tiles
       const double cnt = (double)(n + 1), rest = (double)(N - n - 1);
@@ -172,32 +195,36 @@ __global__ void __launch_bounds__(TB) k_split_loss(const float* __restrict__ A, 
       // constant column: (the value, SSE of the bucket), every row goes right
       double sse = 0.0;
       for (int jj = 0; jj < d; ++jj) sse += s_T2[jj] - s_T1[jj] * s_T1[jj] / (double)N;
-      loss_out[b] = sse;
-      thr_out[b] = keys[s];
+      loss_out[ob] = sse;
+      thr_out[ob] = keys[s];
     } else {
-      loss_out[b] = bl;
-      thr_out[b] = midpoint_threshold(keys[s + bn], keys[s + bn + 1]);
+      loss_out[ob] = bl;
+      thr_out[ob] = midpoint_threshold(keys[s + bn], keys[s + bn + 1]);
     }
   }
 }
 
-// Stable partition of each bucket by x_j >= v_b (L296-302): left child 2b,
-// right child 2b+1, ascending row id kept inside each.
-__global__ void k_partition(const float* __restrict__ A, int64_t lda, const int* __restrict__ perm,
-                            const int* __restrict__ bstart, int col, const float* __restrict__ thr,
-                            int* __restrict__ perm_out, int* __restrict__ nleft_out) {
-  using BS = cub::BlockScan<int, TB>;
+// Stable partition of each bucket by x_j >= v (L296-302): left child 2b,
+// right child 2b+1, ascending row id kept inside each. grid (nb, C).
+__global__ void k_partition(const float* __restrict__ A, int64_t lda, const int* __restrict__ perm_all,
+                            const int* __restrict__ bstart, int Nrows, const int* __restrict__ cols,
+                            const float* __restrict__ thr, int* __restrict__ perm_out_all,
+                            int* __restrict__ nleft_out) {
+  using BSi = cub::BlockScan<int, TB>;
   using BR = cub::BlockReduce<int, TB>;
-  __shared__ typename BS::TempStorage scan_tmp;
+  __shared__ typename BSi::TempStorage scan_tmp;
   __shared__ typename BR::TempStorage red_tmp;
   __shared__ int s_left, s_carry_l, s_carry_r;
-  const int b = blockIdx.x;
-  const int s = bstart[b], e = bstart[b + 1];
-  const float v = thr[b];
+  const int b = blockIdx.x, c = blockIdx.y;
+  const int* perm = perm_all + (size_t)c * Nrows;
+  int* perm_out = perm_out_all + (size_t)c * Nrows;
+  const int col = cols[c];
+  const int s = bstart[c * BS + b], e = bstart[c * BS + b + 1];
+  const float v = thr[c * 16 + b];
   int cl = 0;
   for (int i = s + threadIdx.x; i < e; i += TB) cl += (A[(int64_t)perm[i] * lda + col] < v) ? 1 : 0;
   const int nl = BR(red_tmp).Sum(cl);
-  if (threadIdx.x == 0) s_left = nl, s_carry_l = 0, s_carry_r = 0, nleft_out[b] = nl;
+  if (threadIdx.x == 0) s_left = nl, s_carry_l = 0, s_carry_r = 0, nleft_out[c * 16 + b] = nl;
   __syncthreads();
   const int left_total = s_left;
   for (int base = s; base < e; base += TB) {
@@ -207,9 +234,9 @@ __global__ void k_partition(const float* __restrict__ A, int64_t lda, const int*
     const int isl = in && A[(int64_t)r * lda + col] < v ? 1 : 0;
     const int isr = in && !isl ? 1 : 0;
     int pl, pr, al, ar;
-    BS(scan_tmp).ExclusiveSum(isl, pl, al);
+    BSi(scan_tmp).ExclusiveSum(isl, pl, al);
     __syncthreads();
-    BS(scan_tmp).ExclusiveSum(isr, pr, ar);
+    BSi(scan_tmp).ExclusiveSum(isr, pr, ar);
     if (isl) perm_out[s + s_carry_l + pl] = r;
     if (isr) perm_out[s + left_total + s_carry_r + pr] = r;
     __syncthreads();
@@ -218,12 +245,13 @@ __global__ void k_partition(const float* __restrict__ A, int64_t lda, const int*
   }
 }
 
-// codes[row * C + c] = leaf of row for codebook c.
-__global__ void k_leaf_codes(const int* __restrict__ perm, const int* __restrict__ bstart, int c,
+// codes[row * C + c] = leaf of row for codebook c. grid (16, C).
+__global__ void k_leaf_codes(const int* __restrict__ perm, const int* __restrict__ bstart, int N,
                              int C, uint8_t* __restrict__ codes) {
-  const int b = blockIdx.x;
-  for (int i = bstart[b] + threadIdx.x; i < bstart[b + 1]; i += blockDim.x)
-    codes[(int64_t)perm[i] * C + c] = (uint8_t)b;
+  const int b = blockIdx.x, c = blockIdx.y;
+  const int* pc = perm + (size_t)c * N;
+  for (int i = bstart[c * BS + b] + threadIdx.x; i < bstart[c * BS + b + 1]; i += blockDim.x)
+    codes[(int64_t)pc[i] * C + c] = (uint8_t)b;
 }
 
 // G^T G co-occurrence counts (L318): M[(c,k),(c',k')] += 1 per row.
@@ -243,12 +271,13 @@ __global__ void k_gtg(const uint8_t* __restrict__ codes, int N, int C, unsigned*
 // are the contiguous perm range of the final level). Column-major for potrs:
 // out[j * KC + 16c + k]. With bucket means (lambda = 0) the mean is taken
 // over the subspace only and written row-major into P directly.
-__global__ void k_gta(const float* __restrict__ A, int64_t lda, int D, const int* __restrict__ perm,
-                      const int* __restrict__ bstart, int c, int KC, double* __restrict__ GtA) {
+__global__ void k_gta(const float* __restrict__ A, int64_t lda, int D, const int* __restrict__ perm_all,
+                      const int* __restrict__ bstart, int N, int KC, double* __restrict__ GtA) {
   using BR = cub::BlockReduce<double, TB>;
   __shared__ typename BR::TempStorage tmp;
-  const int k = blockIdx.x;
-  const int s = bstart[k], e = bstart[k + 1];
+  const int k = blockIdx.x % 16, c = blockIdx.x / 16;      // grid (16 C, column blocks)
+  const int* perm = perm_all + (size_t)c * N;
+  const int s = bstart[c * BS + k], e = bstart[c * BS + k + 1];
   for (int j = blockIdx.y; j < D; j += gridDim.y) {
     double acc = 0.0;
     for (int i = s + threadIdx.x; i < e; i += TB) acc += (double)A[(int64_t)perm[i] * lda + j];
@@ -320,37 +349,58 @@ cudaError_t train_model(const float* A, int64_t N64, int64_t lda, int D, int C, 
     return cudaSuccess;
   }
   DevBuf buf;
-  int* perm = buf.get<int>(N);
-  int* perm2 = buf.get<int>(N);
-  int* vals = buf.get<int>(N);
-  int* vals_s = buf.get<int>(N);
-  float* keys = buf.get<float>(N);
-  float* keys_s = buf.get<float>(N);
-  int* d_bstart = buf.get<int>(17);
-  int* d_nleft = buf.get<int>(16);
-  double* d_L = buf.get<double>(16 * 64);
-  double* d_loss = buf.get<double>(16);
-  float* d_thr = buf.get<float>(16);
+  const size_t CN = (size_t)C * N;
+  int* perm = buf.get<int>(CN);
+  int* perm2 = buf.get<int>(CN);
+  int* vals = buf.get<int>(CN);
+  int* vals_s = buf.get<int>(CN);
+  float* keys = buf.get<float>(CN);
+  float* keys_s = buf.get<float>(CN);
+  int* d_bstart = buf.get<int>((size_t)C * BS);
+  int* d_nleft = buf.get<int>((size_t)C * 16);
+  int* d_col0 = buf.get<int>(C);
+  int* d_dn = buf.get<int>(C);
+  int* d_cols = buf.get<int>(C);
+  int* d_segb = buf.get<int>((size_t)C * 8);
+  int* d_sege = buf.get<int>((size_t)C * 8);
+  double* d_L = buf.get<double>((size_t)C * 16 * 64);
+  double* d_loss = buf.get<double>((size_t)C * 16);
+  float* d_thr = buf.get<float>((size_t)C * 16);
   uint8_t* d_codes = buf.get<uint8_t>((size_t)N * C);
   unsigned* d_cnt = buf.get<unsigned>((size_t)KC * KC);
   double* d_M = buf.get<double>((size_t)KC * KC);
   double* d_GtA = buf.get<double>((size_t)KC * D);
-  if (!perm || !perm2 || !vals || !vals_s || !keys || !keys_s || !d_bstart || !d_nleft || !d_L ||
-      !d_loss || !d_thr || !d_codes || !d_cnt || !d_M || !d_GtA) {
+  if (!perm || !perm2 || !vals || !vals_s || !keys || !keys_s || !d_bstart || !d_nleft || !d_col0 ||
+      !d_dn || !d_cols || !d_segb || !d_sege || !d_L || !d_loss || !d_thr || !d_codes || !d_cnt ||
+      !d_M || !d_GtA) {
     *err = MDN_ENOMEM;
     return cudaSuccess;
   }
   cudaError_t e = cudaMemset(d_GtA, 0, (size_t)KC * D * sizeof(double));
   if (e != cudaSuccess) return e;
-  std::vector<int> h_perm(N);
-  for (int i = 0; i < N; ++i) h_perm[i] = i;
-  // CUB temp storage (sized for the largest call: N items, 8 segments)
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  auto d2h = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+  };
+  {
+    std::vector<int> h_perm(CN), dn(C);
+    for (int c = 0; c < C; ++c) {
+      dn[c] = se[c] - sb[c];
+      for (int i = 0; i < N; ++i) h_perm[(size_t)c * N + i] = i;
+    }
+    if ((e = h2d(perm, h_perm.data(), CN * 4)) != cudaSuccess) return e;
+    if ((e = h2d(d_col0, sb.data(), C * 4)) != cudaSuccess) return e;
+    if ((e = h2d(d_dn, dn.data(), C * 4)) != cudaSuccess) return e;
+  }
+  // CUB temp storage (sized for the largest call: C N items, 8 C segments)
   size_t cub_bytes = 0;
   for (int nseg : {1, 2, 4, 8}) {
-    size_t b = 0;
-    cub::DeviceSegmentedSort::StableSortPairs(nullptr, b, keys, keys_s, vals, vals_s, N, nseg,
-                                              d_bstart, d_bstart + 1);
-    cub_bytes = std::max(cub_bytes, b);
+    size_t bb = 0;
+    cub::DeviceSegmentedSort::StableSortPairs(nullptr, bb, keys, keys_s, vals, vals_s, (int)CN,
+                                              nseg * C, d_segb, d_sege);
+    cub_bytes = std::max(cub_bytes, bb);
   }
   void* cub_tmp = buf.get<uint8_t>(cub_bytes);
   if (!cub_tmp) {
@@ -359,67 +409,99 @@ cudaError_t train_model(const float* A, int64_t N64, int64_t lda, int D, int C, 
   }
   std::vector<uint16_t> dims((size_t)C * 4);
   std::vector<float> thr((size_t)C * 15, 0.f);
-  const int gk_blocks = std::min(4096, (N + 255) / 256);
-  for (int c = 0; c < C; ++c) {
-    const int col0 = sb[c], d = se[c] - sb[c];
-    if ((e = cudaMemcpy(perm, h_perm.data(), (size_t)N * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-    std::vector<int> bst = {0, N};
-    for (int t = 0; t < 4; ++t) {
-      const int nb = 1 << t;
-      if ((e = cudaMemcpy(d_bstart, bst.data(), (nb + 1) * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-      // candidates (L265): top-4 of L(j) summed over buckets in bucket order
-      k_dim_sse<<<dim3(nb, d), TB>>>(A, lda, perm, d_bstart, col0, d, d_L);
-      std::vector<double> hL((size_t)nb * d);
-      if ((e = cudaMemcpy(hL.data(), d_L, hL.size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+  const int gk_blocks = std::min(1024, (N + 255) / 256);
+  // bucket offsets per codebook, host side: bst[c * BS + b]
+  std::vector<int> bst((size_t)C * BS, 0);
+  for (int c = 0; c < C; ++c) bst[(size_t)c * BS + 1] = N;
+  for (int t = 0; t < 4; ++t) {
+    const int nb = 1 << t;
+    if ((e = h2d(d_bstart, bst.data(), bst.size() * 4)) != cudaSuccess) return e;
+    // candidates (L265): top-4 of L(j) summed over buckets in bucket order
+    k_dim_sse<<<dim3(nb, dmax, C), TB>>>(A, lda, perm, d_bstart, d_col0, d_dn, N, d_L);
+    std::vector<double> hL((size_t)C * 16 * 64);
+    if ((e = d2h(hL.data(), d_L, hL.size() * 8)) != cudaSuccess) return e;
+    std::vector<std::array<int, 4>> cand(C);
+    for (int c = 0; c < C; ++c) {
+      const int d = se[c] - sb[c];
       std::vector<double> L(d, 0.0);
       for (int b = 0; b < nb; ++b)
-        for (int jj = 0; jj < d; ++jj) L[jj] += hL[(size_t)b * d + jj];
+        for (int jj = 0; jj < d; ++jj) L[jj] += hL[((size_t)c * 16 + b) * 64 + jj];
       std::vector<int> order(d);
       for (int jj = 0; jj < d; ++jj) order[jj] = jj;
       std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return L[x] > L[y]; });
-      std::vector<int> cand(order.begin(), order.begin() + std::min(4, d));
-      std::sort(cand.begin(), cand.end());
-      // score each candidate (Alg. 2 l.4-15)
-      double l_min = INFINITY;
-      int j_min = -1;
-      std::vector<float> v_min(nb);
-      for (int jj : cand) {
-        k_gather_keys<<<gk_blocks, 256>>>(A, lda, perm, N, col0 + jj, keys, vals);
-        size_t bytes = cub_bytes;
-        e = cub::DeviceSegmentedSort::StableSortPairs(cub_tmp, bytes, keys, keys_s, vals, vals_s, N, nb,
-                                                      d_bstart, d_bstart + 1);
-        if (e != cudaSuccess) return e;
-        if (dmax <= 16)
-          k_split_loss<16><<<nb, TB>>>(A, lda, keys_s, vals_s, d_bstart, col0, d, d_loss, d_thr);
-        else
-          k_split_loss<64><<<nb, TB>>>(A, lda, keys_s, vals_s, d_bstart, col0, d, d_loss, d_thr);
-        std::vector<double> hl(nb);
-        std::vector<float> hv(nb);
-        if ((e = cudaMemcpy(hl.data(), d_loss, nb * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
-        if ((e = cudaMemcpy(hv.data(), d_thr, nb * 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
-        double l = 0.0;
-        for (int b = 0; b < nb; ++b) l += hl[b];              // L287, bucket order
-        if (l < l_min) l_min = l, j_min = jj, v_min = hv;     // L289 (strict)
-      }
-      dims[(size_t)c * 4 + t] = (uint16_t)(col0 + j_min);
-      for (int b = 0; b < nb; ++b) thr[(size_t)c * 15 + (1 << t) - 1 + b] = v_min[b];
-      // split (L296-302)
-      if ((e = cudaMemcpy(d_thr, v_min.data(), nb * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-      k_partition<<<nb, TB>>>(A, lda, perm, d_bstart, col0 + j_min, d_thr, perm2, d_nleft);
-      std::vector<int> nl(nb);
-      if ((e = cudaMemcpy(nl.data(), d_nleft, nb * 4, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
-      std::vector<int> nbst(2 * nb + 1);
-      for (int b = 0; b < nb; ++b) nbst[2 * b] = bst[b], nbst[2 * b + 1] = bst[b] + nl[b];
-      nbst[2 * nb] = N;
-      bst = nbst;
-      std::swap(perm, perm2);
+      std::vector<int> cs(order.begin(), order.begin() + std::min(4, d));
+      std::sort(cs.begin(), cs.end());
+      for (int q = 0; q < 4; ++q) cand[c][q] = cs[std::min(q, (int)cs.size() - 1)];   // pad: re-evaluation ties, kept out by L289's strict <
     }
-    // leaves -> codes (R12: membership == re-encoding under R9) and G^T A~
-    if ((e = cudaMemcpy(d_bstart, bst.data(), 17 * 4, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-    k_leaf_codes<<<16, 256>>>(perm, d_bstart, c, C, d_codes);
-    k_gta<<<dim3(16, std::min(D, 1024)), TB>>>(A, lda, D, perm, d_bstart, c, KC, d_GtA);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // segments of the sort: bucket b of codebook c
+    {
+      std::vector<int> sbg((size_t)C * nb), seg((size_t)C * nb);
+      for (int c = 0; c < C; ++c)
+        for (int b = 0; b < nb; ++b) {
+          sbg[(size_t)c * nb + b] = (int)((size_t)c * N + bst[(size_t)c * BS + b]);
+          seg[(size_t)c * nb + b] = (int)((size_t)c * N + bst[(size_t)c * BS + b + 1]);
+        }
+      if ((e = h2d(d_segb, sbg.data(), sbg.size() * 4)) != cudaSuccess) return e;
+      if ((e = h2d(d_sege, seg.data(), seg.size() * 4)) != cudaSuccess) return e;
+    }
+    // score each candidate (Alg. 2 l.4-15), all codebooks at once
+    std::vector<double> l_min(C, INFINITY);
+    std::vector<int> j_min(C, -1);
+    std::vector<float> v_min((size_t)C * 16, 0.f);
+    for (int q = 0; q < 4; ++q) {
+      std::vector<int> cols(C);
+      for (int c = 0; c < C; ++c) cols[c] = sb[c] + cand[c][q];
+      if ((e = h2d(d_cols, cols.data(), C * 4)) != cudaSuccess) return e;
+      k_gather_keys<<<dim3(gk_blocks, C), 256>>>(A, lda, perm, N, d_cols, keys, vals);
+      size_t bytes = cub_bytes;
+      e = cub::DeviceSegmentedSort::StableSortPairs(cub_tmp, bytes, keys, keys_s, vals, vals_s, (int)CN,
+                                                    nb * C, d_segb, d_sege);
+      if (e != cudaSuccess) return e;
+      if (dmax <= 16)
+        k_split_loss<16><<<dim3(nb, C), TB>>>(A, lda, keys_s, vals_s, d_bstart, d_col0, d_dn, N, d_loss, d_thr);
+      else
+        k_split_loss<64><<<dim3(nb, C), TB>>>(A, lda, keys_s, vals_s, d_bstart, d_col0, d_dn, N, d_loss, d_thr);
+      std::vector<double> hl((size_t)C * 16);
+      std::vector<float> hv((size_t)C * 16);
+      if ((e = d2h(hl.data(), d_loss, hl.size() * 8)) != cudaSuccess) return e;
+      if ((e = d2h(hv.data(), d_thr, hv.size() * 4)) != cudaSuccess) return e;
+      for (int c = 0; c < C; ++c) {
+        double l = 0.0;
+        for (int b = 0; b < nb; ++b) l += hl[(size_t)c * 16 + b];          // L287, bucket order
+        if (l < l_min[c]) {                                                  // L289 (strict)
+          l_min[c] = l, j_min[c] = cand[c][q];
+          for (int b = 0; b < nb; ++b) v_min[(size_t)c * 16 + b] = hv[(size_t)c * 16 + b];
+        }
+      }
+    }
+    std::vector<int> cols(C);
+    for (int c = 0; c < C; ++c) {
+      cols[c] = sb[c] + j_min[c];
+      dims[(size_t)c * 4 + t] = (uint16_t)cols[c];
+      for (int b = 0; b < nb; ++b) thr[(size_t)c * 15 + (1 << t) - 1 + b] = v_min[(size_t)c * 16 + b];
+    }
+    // split (L296-302)
+    if ((e = h2d(d_cols, cols.data(), C * 4)) != cudaSuccess) return e;
+    if ((e = h2d(d_thr, v_min.data(), v_min.size() * 4)) != cudaSuccess) return e;
+    k_partition<<<dim3(nb, C), TB>>>(A, lda, perm, d_bstart, N, d_cols, d_thr, perm2, d_nleft);
+    std::vector<int> nl((size_t)C * 16);
+    if ((e = d2h(nl.data(), d_nleft, nl.size() * 4)) != cudaSuccess) return e;
+    std::vector<int> nbst((size_t)C * BS, 0);
+    for (int c = 0; c < C; ++c) {
+      for (int b = 0; b < nb; ++b) {
+        nbst[(size_t)c * BS + 2 * b] = bst[(size_t)c * BS + b];
+        nbst[(size_t)c * BS + 2 * b + 1] = bst[(size_t)c * BS + b] + nl[(size_t)c * 16 + b];
+      }
+      nbst[(size_t)c * BS + 2 * nb] = N;
+    }
+    bst.swap(nbst);
+    std::swap(perm, perm2);
   }
+  // leaves -> codes (R12: membership == re-encoding under R9) and G^T A~
+  if ((e = h2d(d_bstart, bst.data(), bst.size() * 4)) != cudaSuccess) return e;
+  k_leaf_codes<<<dim3(16, C), 256>>>(perm, d_bstart, N, C, d_codes);
+  k_gta<<<dim3(16 * C, std::min(D, 256)), TB>>>(A, lda, D, perm, d_bstart, N, KC, d_GtA);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // prototypes
   std::vector<float> P((size_t)KC * D, 0.f);
   std::vector<double> X((size_t)KC * D);
