@@ -101,10 +101,10 @@ __device__ __forceinline__ uint32_t tree_code(V x0, V x1, V x2, V x3, const V (&
 //   lt_t = [x_t < v_t] = 1 - b_t is the sign bit of x_t - v_t;
 //   n_{t+1} = 2 n_t + lt_t is the complemented node index (n_4 = 15 - code).
 //   Levels 2 and 3 pick their threshold with PRMT from the byte-packed level
-//   table (complemented node order), selector n * 0x11: bytes 0 and 1 hold the
-//   threshold, bytes 2 and 3 byte 0 of the table (g); the split value is
-//   packed the same way (x, x, g, g), so the word difference is (x - v) * 257
-//   and its sign is the compare.
+//   table (complemented node order) with selector n: byte 0 holds the
+//   threshold, bytes 1-3 byte 0 of the table (g); the split value is packed
+//   the same way (x, g, g, g), so the word difference is x - v and its sign
+//   is the compare.
 struct ByteTree {
   int q0, q2, d12;                 // level 0 threshold; level 1: v = q2 + lt0 * (q1 - q2)
   uint32_t Q2, Q3lo, Q3hi;         // level tables, byte n = threshold of complemented node n
@@ -127,16 +127,20 @@ __device__ __forceinline__ uint32_t sign_bit(uint32_t x) {
   return d;
 }
 
+// n' = 2n + [d < 0] in one funnel shift: the upper word of {n, d} << 1.
+__device__ __forceinline__ uint32_t push_sign(uint32_t n, uint32_t d) {
+  uint32_t r;
+  asm("shf.l.wrap.b32 %0, %1, %2, 1;" : "=r"(r) : "r"(d), "r"(n));
+  return r;
+}
+
 template <int W2>
 __device__ __forceinline__ uint32_t byte_tree_addr(uint32_t w, const ByteTree& b) {
   const uint32_t lt0 = sign_bit(prmt(w, 0u, b.s0) - (uint32_t)b.q0);
   const uint32_t v1 = (uint32_t)b.q2 + lt0 * (uint32_t)b.d12;
-  const uint32_t lt1 = sign_bit(prmt(w, 0u, b.s1) - v1);
-  const uint32_t n2 = 2u * lt0 + lt1;
-  const uint32_t lt2 = sign_bit(prmt(w, b.g2, b.s2) - prmt(b.Q2, b.Q2, n2 * 0x11u));
-  const uint32_t n3 = 2u * n2 + lt2;
-  const uint32_t lt3 = sign_bit(prmt(w, b.g3, b.s3) - prmt(b.Q3lo, b.Q3hi, n3 * 0x11u));
-  const uint32_t n4 = 2u * n3 + lt3;               // 15 - code
+  const uint32_t n2 = push_sign(lt0, prmt(w, 0u, b.s1) - v1);
+  const uint32_t n3 = push_sign(n2, prmt(w, b.g2, b.s2) - prmt(b.Q2, b.Q2, n2));
+  const uint32_t n4 = push_sign(n3, prmt(w, b.g3, b.s3) - prmt(b.Q3lo, b.Q3hi, n3));   // 15 - code
   return b.base - n4 * (4u * W2);
 }
 
@@ -254,8 +258,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t j0 = o[0] - sub, j1 = o[1] - sub, j2 = o[2] - sub, j3 = o[3] - sub;
     bt.s0 = j0 | 0x4440u;
     bt.s1 = j1 | 0x4440u;
-    bt.s2 = j2 | (j2 << 4) | 0x4400u;
-    bt.s3 = j3 | (j3 << 4) | 0x4400u;
+    bt.s2 = j2 | 0x4440u;                          // (x, g, g, g)
+    bt.s3 = j3 | 0x4440u;
     bt.base = lut_c + 15u * 4u * W2;
   }
   int s = grp, ph = 0;
