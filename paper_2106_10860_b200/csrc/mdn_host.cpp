@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <memory>
 #include <new>
@@ -76,6 +77,8 @@ void put(std::vector<uint8_t>& o, T v) {
 
 int cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return MDN_OK;
+  static const bool debug = getenv("MDN_DEBUG") != nullptr;
+  if (debug) fprintf(stderr, "libmaddness: CUDA error %d: %s\n", (int)e, cudaGetErrorString(e));
   if (e == cudaErrorMemoryAllocation) return MDN_ENOMEM;
   return MDN_ECUDA;
 }
