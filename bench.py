@@ -471,7 +471,7 @@ def run(args):
     if op == "amm" and not u8 and not col and not pq and (rank == 0 or ws > 1):
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
                                  n_slots=3)
-        n_e2e = min(n, (1 << 32) // (4 * spec.D))     # <= 4 GiB of pinned host A per rank
+        n_e2e = min(n, (1 << 30) // (4 * spec.D))     # <= 1 GiB of pinned host A per rank
         A_h = A[:n_e2e].cpu().pin_memory()
         out_h = torch.empty((n_e2e, spec.M), dtype=torch.float32).pin_memory()
         mdn.mdn_amm_host(ex, A_h, out_h)                      # warm-up

@@ -125,3 +125,28 @@ def test_no_unresolved_symbols(lib):
                          text=True).stdout.split("\n")
     bad = [l for l in out if l.strip().startswith("U ") and "@" not in l]
     assert not bad, bad
+
+
+def test_train_size_query_and_argument_errors(lib):
+    """mdn_train's size query (buf == NULL) needs no device; bad shapes fail
+    before any device work."""
+    n = ct.c_size_t(0)
+    lib.mdn_train.argtypes = [ct.c_void_p, ct.c_int64, ct.c_int64, ct.c_int, ct.c_int, ct.c_double,
+                              ct.c_int, ct.c_void_p, ct.POINTER(ct.c_size_t)]
+    assert lib.mdn_train(None, 0, 0, 512, 32, 1.0, 0, None, ct.byref(n)) == 0
+    assert n.value == 48 + 76 * 32 + 64 * 32 * 512 + 8          # == len(cls100.mdnm)
+    assert n.value == len(model_bytes("cls100"))
+    assert lib.mdn_train(None, 0, 0, 8, 9, 1.0, 0, None, ct.byref(n)) == -1      # C > D
+    assert lib.mdn_train(None, 0, 0, 8, 4, -1.0, 0, None, ct.byref(n)) == -1     # lambda < 0
+    buf = ct.create_string_buffer(16)
+    n = ct.c_size_t(16)
+    assert lib.mdn_train(None, 10, 8, 8, 4, 1.0, 0, buf, ct.byref(n)) == -1      # capacity too small
+
+
+def test_bench_split_dims_parser():
+    """bench.py's independent model-header parser agrees with the oracle's reader."""
+    import bench
+    import oracle as O
+    for name in ("tiny", "cls100", "scale"):
+        blob = model_bytes(name)
+        assert bench.split_dims(blob) == sorted(set(O.read_model(blob).dims.reshape(-1).tolist()))
