@@ -121,13 +121,16 @@ def _metric(name):
     return f"MADDNESS encode+scan rows/s and % HBM peak ({name}: D={sp.D},M={sp.M},C={sp.C})"
 
 
-def _bench_rows(name, rank, ws, device):
-    """This rank's shard of the config's bench-size A (weak scaling)."""
+def _bench_rows(name, rank, ws, device, strong=False):
+    """This rank's shard of the config's bench-size A: n_bench rows per GPU
+    (weak scaling, default) or n_bench rows in total split over the GPUs
+    (strong scaling: config 5's "rows sharded across 1/2/4/8 B200")."""
     from datagen.synth import CHUNK_ROWS, CONFIGS, make_config_data, relu_W, relu_lowrank_torch
     from paper_2106_10860_b200.dist import shard_rows
     spec = CONFIGS[name]
     if spec.kind == "relu":
-        _, n, first_chunk = shard_rows(rank, ws, spec.n_bench, CHUNK_ROWS)
+        per_rank = spec.n_bench // ws if strong else spec.n_bench
+        _, n, first_chunk = shard_rows(rank, ws, per_rank, CHUNK_ROWS)
         return relu_lowrank_torch(relu_W(name), n, first_chunk, device)
     import torch
     _, A, _ = make_config_data(name, n_test=spec.n_test, n_train=0)   # 4M patches (f32 or u8), tiled
@@ -327,7 +330,7 @@ def run(args):
     luts = mdn.mdn_luts_load(luts_blob, dev)
 
     # --- this rank's shard of A (2^21 rows, chunks rank*2 .. rank*2+1) --------
-    A = _bench_rows(name, rank, ws, "cuda")
+    A = _bench_rows(name, rank, ws, "cuda", strong=args.strong)
     n = A.shape[0]
     out = torch.empty((n, spec.M), dtype=torch.float32, device="cuda")
     stream = torch.cuda.Stream()
@@ -524,7 +527,8 @@ def run(args):
             "value": value,
             "unit": "rows/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+            "vs_baseline": None, "dtype": "u8",
             "data": "synthetic",
             "config": {"workload": f"{name}: D={spec.D}, M={spec.M}, C={spec.C}, K=16, {args.mode} sum"
                        + (f" (U={spec.U})" if args.mode == "avg" else "")
@@ -574,6 +578,9 @@ def main():
     ap.add_argument("--op", choices=["amm", "encode", "scan", "train"], default="amm",
                     help="amm (the hot path, default), the unfused halves, or train: GPU "
                          "training (SURVEY N3) on the config's training split, for DESIGN.md")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the config's bench rows in total, split over the GPUs "
+                         "(relu configs; e.g. --config scale = BASELINE config 5)")
     ap.add_argument("--encoder", choices=["maddness", "pq"], default="maddness",
                     help="maddness (the method) or pq: the PQ comparator encoder (SURVEY N4) "
                          "feeding the same scan")
