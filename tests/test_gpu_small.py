@@ -109,3 +109,35 @@ def test_u8_split_value_256_uses_integer_tree(mdn):
         out = torch.empty((A.shape[0], 2), device="cuda")
         mdn.mdn_amm_u8(model, luts, torch.from_numpy(A).cuda(), out)
         assert (_bits(out.cpu().numpy()) == _bits(want)).all()
+
+
+@pytest.mark.parametrize("name", ["tiny", "image", "image_u8"])
+def test_bench_size_sampled_parity(mdn, name):
+    """The register-tree kernels at the bench size, built exactly as bench.py
+    builds them (tiny: 2^25 generated rows; image / image_u8: the 4M test
+    patches tiled x8 = 32M rows); 65536 sampled rows + the tail vs the oracle."""
+    import bench
+    from datagen.synth import CONFIGS
+    spec = CONFIGS[name]
+    blob = model_bytes(name)
+    om = O.read_model(blob)
+    model = mdn.mdn_model_load(blob, 0)
+    B = bench._config_B(name)
+    A = bench._bench_rows(name, 0, 1, "cuda")
+    n = A.shape[0]
+    rng = np.random.default_rng(77)
+    rows = np.unique(np.concatenate([rng.integers(0, n, 65536), np.arange(n - 300, n)]))
+    idx = torch.from_numpy(rows).cuda()
+    As = A.index_select(0, idx).cpu().numpy()
+    u8 = A.dtype == torch.uint8
+    for mode, mi in (("exact", 0), ("avg", 1)):
+        luts = mdn.mdn_build_luts(model, B, mi, spec.U)
+        out = torch.empty((n, spec.M), device="cuda")
+        (mdn.mdn_amm_u8 if u8 else mdn.mdn_amm)(model, luts, A, out)
+        torch.cuda.synchronize()
+        got = out.index_select(0, idx).cpu().numpy()
+        want = (O.amm_u8 if u8 else O.amm)(As, om, O.make_luts(om, B, mode, spec.U))[2]
+        assert (_bits(got) == _bits(want)).all()
+        del out
+    del A
+    torch.cuda.empty_cache()
