@@ -108,56 +108,98 @@ __device__ __forceinline__ float midpoint_threshold(float a, float b) {
   return v;
 }
 
-// Algorithm 3 on every bucket of every codebook for one candidate column each.
-// Rows of bucket b of codebook c are keys/vals[c N + bstart[c BS + b] ..) sorted
-// by x_j. grid (nb, C); outputs per (c, b) the loss of the best realisable
-// split and its threshold.
-template <int DMAX>
-__global__ void __launch_bounds__(TB) k_split_loss(const float* __restrict__ A, int64_t lda,
-                                                   const float* __restrict__ keys_all,
-                                                   const int* __restrict__ vals_all,
-                                                   const int* __restrict__ bstart,
-                                                   const int* __restrict__ col0_a,
-                                                   const int* __restrict__ dims_n, int Nrows,
-                                                   double* __restrict__ loss_out,
-                                                   float* __restrict__ thr_out) {
-  using BSc = cub::BlockScan<double, TB>;
+// Algorithm 3 on every bucket of every codebook for one candidate column each,
+// split over row tiles of TR rows so large buckets use many CTAs. Rows of
+// bucket b of codebook c are keys/vals[c N + bstart[c BS + b] ..) sorted by x_j.
+//   k_tile_sums      per (codebook, bucket, tile, dim): sum x, sum x^2
+//   k_split_tiles    per tile: prefix sums = earlier tiles' sums (ascending) +
+//                    in-tile block scans; the loss of every realisable
+//                    position (Alg. 3 L634-635 with Alg. 4, dims
+//                    ascending); the tile's first minimum
+//   k_split_reduce   per bucket: first minimum over the tiles (R8), the
+//                    threshold (R9) or the constant-column / empty cases
+constexpr int TR = 4096;   // rows per tile
+constexpr int DS = 64;     // per-dim stride of the tile sums (max subspace width)
+
+__device__ __forceinline__ void bucket_range(const int* bstart, int c, int b, int tile, int& s,
+                                             int& e, int& start, int& end) {
+  s = bstart[c * BS + b], e = bstart[c * BS + b + 1];
+  start = s + tile * TR;
+  end = min(start + TR, e);
+}
+
+__global__ void __launch_bounds__(TB) k_tile_sums(const float* __restrict__ A, int64_t lda,
+                                                  const int* __restrict__ vals_all,
+                                                  const int* __restrict__ bstart,
+                                                  const int* __restrict__ col0_a,
+                                                  const int* __restrict__ dims_n, int Nrows, int Tmax,
+                                                  double* __restrict__ tsum) {
   using BR = cub::BlockReduce<double, TB>;
-  __shared__ typename BSc::TempStorage scan_tmp;
-  __shared__ typename BR::TempStorage red_tmp;
-  __shared__ double s_T1[DMAX], s_T2[DMAX], s_c1[DMAX], s_c2[DMAX];
-  __shared__ double s_bl[TB];
-  __shared__ int s_bn[TB];
-  const int b = blockIdx.x, c = blockIdx.y;
-  const float* keys = keys_all + (size_t)c * Nrows;
+  __shared__ typename BR::TempStorage tmp;
+  const int tile = blockIdx.x, b = blockIdx.y, c = blockIdx.z;
+  int s, e, start, end;
+  bucket_range(bstart, c, b, tile, s, e, start, end);
+  if (start >= e) return;
   const int* vals = vals_all + (size_t)c * Nrows;
   const int col0 = col0_a[c], d = dims_n[c];
-  const int s = bstart[c * BS + b], e = bstart[c * BS + b + 1], N = e - s;
-  const int ob = c * 16 + b;
-  if (N == 0) {                                            // R10
-    if (threadIdx.x == 0) loss_out[ob] = 0.0, thr_out[ob] = 0.f;
-    return;
-  }
-  // bucket totals per dim (for the suffix sums: tail = total - prefix)
+  double* out = tsum + (((size_t)c * 16 + b) * Tmax + tile) * DS * 2;
   for (int jj = 0; jj < d; ++jj) {
     double a1 = 0.0, a2 = 0.0;
-    for (int i = s + threadIdx.x; i < e; i += TB) {
+    for (int i = start + threadIdx.x; i < end; i += TB) {
       const double x = (double)A[(int64_t)vals[i] * lda + col0 + jj];
       a1 += x, a2 += x * x;
     }
-    const double t1 = BR(red_tmp).Sum(a1);
+    const double t1 = BR(tmp).Sum(a1);
     __syncthreads();
-    const double t2 = BR(red_tmp).Sum(a2);
-    if (threadIdx.x == 0) s_T1[jj] = t1, s_T2[jj] = t2, s_c1[jj] = 0.0, s_c2[jj] = 0.0;
+    const double t2 = BR(tmp).Sum(a2);
+    if (threadIdx.x == 0) out[2 * jj] = t1, out[2 * jj + 1] = t2;
     __syncthreads();
   }
+}
+
+template <int DMAX>
+__global__ void __launch_bounds__(TB) k_split_tiles(const float* __restrict__ A, int64_t lda,
+                                                    const float* __restrict__ keys_all,
+                                                    const int* __restrict__ vals_all,
+                                                    const int* __restrict__ bstart,
+                                                    const int* __restrict__ col0_a,
+                                                    const int* __restrict__ dims_n, int Nrows,
+                                                    int Tmax, const double* __restrict__ tsum,
+                                                    double* __restrict__ tbest_l,
+                                                    int* __restrict__ tbest_n) {
+  using BSc = cub::BlockScan<double, TB>;
+  __shared__ typename BSc::TempStorage scan_tmp;
+  __shared__ double s_T1[DMAX], s_T2[DMAX], s_c1[DMAX], s_c2[DMAX];
+  __shared__ double s_bl[TB];
+  __shared__ int s_bn[TB];
+  const int tile = blockIdx.x, b = blockIdx.y, c = blockIdx.z;
+  int s, e, start, end;
+  bucket_range(bstart, c, b, tile, s, e, start, end);
+  if (start >= e) return;
+  const float* keys = keys_all + (size_t)c * Nrows;
+  const int* vals = vals_all + (size_t)c * Nrows;
+  const int col0 = col0_a[c], d = dims_n[c];
+  const int N = e - s;
+  const int ntiles = (N + TR - 1) / TR;
+  const double* ts = tsum + ((size_t)c * 16 + b) * Tmax * DS * 2;
+  for (int jj = threadIdx.x; jj < d; jj += TB) {          // carry-in and totals, tiles ascending
+    double c1 = 0.0, c2 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int t = 0; t < ntiles; ++t) {
+      const double v1 = ts[(size_t)t * DS * 2 + 2 * jj], v2 = ts[(size_t)t * DS * 2 + 2 * jj + 1];
+      if (t < tile) c1 += v1, c2 += v2;
+      t1 += v1, t2 += v2;
+    }
+    s_c1[jj] = c1, s_c2[jj] = c2, s_T1[jj] = t1, s_T2[jj] = t2;
+  }
+  __syncthreads();
   double best = INFINITY;
   int best_n = -1;
-  for (int base = 0; base < N; base += TB) {
-    const int n = base + threadIdx.x;                       // position in the bucket (0-based)
-    const bool in = n < N;
-    const bool valid = n + 1 < N && keys[s + n] < keys[s + n + 1];   // R7 + R9
-    const int row = in ? vals[s + n] : 0;
+  for (int base = start; base < end; base += TB) {
+    const int i = base + threadIdx.x;                      // absolute index in keys / vals
+    const int n = i - s;                                   // position in the bucket (0-based)
+    const bool in = i < end;
+    const bool valid = in && n + 1 < N && keys[i] < keys[i + 1];     // R7 + R9
+    const int row = in ? vals[i] : 0;
     double head = 0.0, tail = 0.0;
     for (int jj = 0; jj < d; ++jj) {
       const double x = in ? (double)A[(int64_t)row * lda + col0 + jj] : 0.0;
@@ -166,10 +208,10 @@ __global__ void __launch_bounds__(TB) k_split_loss(const float* __restrict__ A, 
       __syncthreads();
       BSc(scan_tmp).InclusiveSum(x * x, p2, agg2);
       __syncthreads();
-      p1 += s_c1[jj], p2 += s_c2[jj];                       // carry from earlier tiles
+      p1 += s_c1[jj], p2 += s_c2[jj];
       const double cnt = (double)(n + 1), rest = (double)(N - n - 1);
-      head += p2 - p1 * p1 / cnt;                           // Alg. 4, dims ascending
-      if (rest > 1) {                                       // rest == 1: L662's out[0] = 0
+      head += p2 - p1 * p1 / cnt;                          // Alg. 4, dims ascending
+      if (rest > 1) {                                      // rest == 1: L662's out[0] = 0
         const double r1 = s_T1[jj] - p1, r2 = s_T2[jj] - p2;
         tail += r2 - r1 * r1 / rest;
       }
@@ -177,10 +219,10 @@ __global__ void __launch_bounds__(TB) k_split_loss(const float* __restrict__ A, 
       if (threadIdx.x == TB - 1) s_c1[jj] += agg1, s_c2[jj] += agg2;
       __syncthreads();
     }
-    if (n == 0) head = 0.0;                                 // L662: out[0] = 0
+    if (n == 0) head = 0.0;                                // L662: out[0] = 0
     if (valid) {
-      const double l = head + tail;                         // L634-635
-      if (l < best) best = l, best_n = n;                   // ascending n: first minimum
+      const double l = head + tail;                        // L634-635
+      if (l < best) best = l, best_n = n;
     }
   }
   s_bl[threadIdx.x] = best;
@@ -189,18 +231,49 @@ __global__ void __launch_bounds__(TB) k_split_loss(const float* __restrict__ A, 
   if (threadIdx.x == 0) {
     double bl = INFINITY;
     int bn = -1;
-    for (int t = 0; t < TB; ++t)                            // lowest position on ties (R8)
+    for (int t = 0; t < TB; ++t)                           // lowest position on ties (R8)
       if (s_bn[t] >= 0 && (s_bl[t] < bl || (s_bl[t] == bl && s_bn[t] < bn))) bl = s_bl[t], bn = s_bn[t];
-    if (bn < 0) {
-      // constant column: (the value, SSE of the bucket), every row goes right
-      double sse = 0.0;
-      for (int jj = 0; jj < d; ++jj) sse += s_T2[jj] - s_T1[jj] * s_T1[jj] / (double)N;
-      loss_out[ob] = sse;
-      thr_out[ob] = keys[s];
-    } else {
-      loss_out[ob] = bl;
-      thr_out[ob] = midpoint_threshold(keys[s + bn], keys[s + bn + 1]);
+    const size_t o = ((size_t)c * 16 + b) * Tmax + tile;
+    tbest_l[o] = bl;
+    tbest_n[o] = bn;
+  }
+}
+
+__global__ void k_split_reduce(const float* __restrict__ keys_all, const int* __restrict__ bstart,
+                               const int* __restrict__ dims_n, int Nrows, int Tmax,
+                               const double* __restrict__ tsum, const double* __restrict__ tbest_l,
+                               const int* __restrict__ tbest_n, double* __restrict__ loss_out,
+                               float* __restrict__ thr_out) {
+  const int b = blockIdx.x, c = blockIdx.y;
+  if (threadIdx.x != 0) return;
+  const int s = bstart[c * BS + b], e = bstart[c * BS + b + 1], N = e - s;
+  const int ob = c * 16 + b;
+  if (N == 0) {                                            // R10
+    loss_out[ob] = 0.0, thr_out[ob] = 0.f;
+    return;
+  }
+  const float* keys = keys_all + (size_t)c * Nrows;
+  const int ntiles = (N + TR - 1) / TR;
+  double bl = INFINITY;
+  int bn = -1;
+  for (int t = 0; t < ntiles; ++t) {                       // tiles ascending: strict < keeps the first
+    const size_t o = (size_t)ob * Tmax + t;
+    if (tbest_n[o] >= 0 && tbest_l[o] < bl) bl = tbest_l[o], bn = tbest_n[o];
+  }
+  if (bn < 0) {
+    // constant column: (the value, SSE of the bucket), every row goes right
+    const double* ts = tsum + (size_t)ob * Tmax * DS * 2;
+    double sse = 0.0;
+    for (int jj = 0; jj < dims_n[c]; ++jj) {
+      double t1 = 0.0, t2 = 0.0;
+      for (int t = 0; t < ntiles; ++t) t1 += ts[(size_t)t * DS * 2 + 2 * jj], t2 += ts[(size_t)t * DS * 2 + 2 * jj + 1];
+      sse += t2 - t1 * t1 / (double)N;
     }
+    loss_out[ob] = sse;
+    thr_out[ob] = keys[s];
+  } else {
+    loss_out[ob] = bl;
+    thr_out[ob] = midpoint_threshold(keys[s + bn], keys[s + bn + 1]);
   }
 }
 
@@ -365,6 +438,10 @@ cudaError_t train_model(const float* A, int64_t N64, int64_t lda, int D, int C, 
   int* d_sege = buf.get<int>((size_t)C * 8);
   double* d_L = buf.get<double>((size_t)C * 16 * 64);
   double* d_loss = buf.get<double>((size_t)C * 16);
+  const int Tmax = (N + TR - 1) / TR;
+  double* d_tsum = buf.get<double>((size_t)C * 16 * Tmax * DS * 2);
+  double* d_tbl = buf.get<double>((size_t)C * 16 * Tmax);
+  int* d_tbn = buf.get<int>((size_t)C * 16 * Tmax);
   float* d_thr = buf.get<float>((size_t)C * 16);
   uint8_t* d_codes = buf.get<uint8_t>((size_t)N * C);
   unsigned* d_cnt = buf.get<unsigned>((size_t)KC * KC);
@@ -372,7 +449,7 @@ cudaError_t train_model(const float* A, int64_t N64, int64_t lda, int D, int C, 
   double* d_GtA = buf.get<double>((size_t)KC * D);
   if (!perm || !perm2 || !vals || !vals_s || !keys || !keys_s || !d_bstart || !d_nleft || !d_col0 ||
       !d_dn || !d_cols || !d_segb || !d_sege || !d_L || !d_loss || !d_thr || !d_codes || !d_cnt ||
-      !d_M || !d_GtA) {
+      !d_M || !d_GtA || !d_tsum || !d_tbl || !d_tbn) {
     *err = MDN_ENOMEM;
     return cudaSuccess;
   }
@@ -444,6 +521,10 @@ cudaError_t train_model(const float* A, int64_t N64, int64_t lda, int D, int C, 
       if ((e = h2d(d_segb, sbg.data(), sbg.size() * 4)) != cudaSuccess) return e;
       if ((e = h2d(d_sege, seg.data(), seg.size() * 4)) != cudaSuccess) return e;
     }
+    int tiles_lv = 1;                                  // tiles of the largest bucket
+    for (int c = 0; c < C; ++c)
+      for (int b = 0; b < nb; ++b)
+        tiles_lv = std::max(tiles_lv, (bst[(size_t)c * BS + b + 1] - bst[(size_t)c * BS + b] + TR - 1) / TR);
     // score each candidate (Alg. 2 l.4-15), all codebooks at once
     std::vector<double> l_min(C, INFINITY);
     std::vector<int> j_min(C, -1);
@@ -457,10 +538,16 @@ cudaError_t train_model(const float* A, int64_t N64, int64_t lda, int D, int C, 
       e = cub::DeviceSegmentedSort::StableSortPairs(cub_tmp, bytes, keys, keys_s, vals, vals_s, (int)CN,
                                                     nb * C, d_segb, d_sege);
       if (e != cudaSuccess) return e;
+      const dim3 tg(tiles_lv, nb, C);
+      k_tile_sums<<<tg, TB>>>(A, lda, vals_s, d_bstart, d_col0, d_dn, N, Tmax, d_tsum);
       if (dmax <= 16)
-        k_split_loss<16><<<dim3(nb, C), TB>>>(A, lda, keys_s, vals_s, d_bstart, d_col0, d_dn, N, d_loss, d_thr);
+        k_split_tiles<16><<<tg, TB>>>(A, lda, keys_s, vals_s, d_bstart, d_col0, d_dn, N, Tmax, d_tsum,
+                                      d_tbl, d_tbn);
       else
-        k_split_loss<64><<<dim3(nb, C), TB>>>(A, lda, keys_s, vals_s, d_bstart, d_col0, d_dn, N, d_loss, d_thr);
+        k_split_tiles<64><<<tg, TB>>>(A, lda, keys_s, vals_s, d_bstart, d_col0, d_dn, N, Tmax, d_tsum,
+                                      d_tbl, d_tbn);
+      k_split_reduce<<<dim3(nb, C), 32>>>(keys_s, d_bstart, d_dn, N, Tmax, d_tsum, d_tbl, d_tbn, d_loss,
+                                          d_thr);
       std::vector<double> hl((size_t)C * 16);
       std::vector<float> hv((size_t)C * 16);
       if ((e = d2h(hl.data(), d_loss, hl.size() * 8)) != cudaSuccess) return e;
