@@ -5,9 +5,9 @@
   and the ridge prototypes agree to the Cholesky's rounding.
 * fp32 data: block-parallel prefix sums add in another order than the
   oracle's sequential cumsum, so a split may differ where two candidates tie
-  within rounding; the realised per-level losses of the GPU trees must match
-  the oracle's to 1e-9 relative (both are optimal to rounding), and almost all
-  thresholds must coincide.
+  within rounding; the contract is that the realised per-level losses match
+  the oracle's to 1e-9 relative. On the fixed test inputs the trees are in
+  fact identical.
 """
 import numpy as np
 import pytest
@@ -59,17 +59,19 @@ def test_train_integer_data_bit_exact_trees(mdn):
 
 
 @pytest.mark.parametrize("name,C", [("tiny", 4), ("cls10_c16", 16)])
-def test_train_fp32_data_optimal_to_rounding(mdn, name, C):
+def test_train_fp32_data(mdn, name, C):
+    """fp32 rows: the realised per-level losses match the oracle's to 1e-9
+    (the contract: a split tying another within rounding may legitimately
+    differ), and on these fixed inputs the trees are in fact identical (as on
+    cls100 and scale, measured: DESIGN.md), with prototypes to 1e-6."""
     A = make_config_data(name, n_test=0, n_train=20_000 if name != "tiny" else 4096)[0]
     want = O.train(A, C, lam=1.0)
     got = _gpu_train(mdn, A, C, 1.0)
     lw, lg = _level_losses(A, want), _level_losses(A, got)
     assert np.allclose(lg, lw, rtol=1e-9, atol=0), np.abs(lg - lw).max()
-    same = (got.thr.view(np.uint32) == want.thr.view(np.uint32)).mean()
-    assert same >= 0.95, same
-    # where the trees agree, so do the ridge prototypes (same G, same A~)
-    if (got.dims == want.dims).all() and (got.thr == want.thr).all():
-        assert np.abs(got.P.astype(np.float64) - want.P).max() <= 1e-4 * np.abs(want.P).max()
+    assert (got.dims == want.dims).all()
+    assert (got.thr.view(np.uint32) == want.thr.view(np.uint32)).all()
+    assert np.abs(got.P.astype(np.float64) - want.P).max() <= 1e-6 * np.abs(want.P).max()
 
 
 def test_train_bucket_means(mdn):
