@@ -9,9 +9,10 @@
 // HBM bytes per row are 4 |S| + 4M (|S| = distinct split dims) instead of
 // 4D + 4M: 912 vs 2448 for the CIFAR-100-shaped config.
 //
-// The fused path for heavy scans (W >= 8 table words per code) runs the
-// warp-specialised TMA kernel of mdn_fast.cu with a [slot][row] stage layout
-// (launch_amm_ws_cm); everything else runs here.
+// The fused path runs the warp-specialised TMA kernel of mdn_fast.cu with a
+// [slot][row] stage layout filled by TMA gather4 (launch_amm_ws_cm) whenever
+// its shapes are supported; the thread-per-row kernel here is the fallback
+// and the encode-only path.
 //
 // k_amm_cm: thread per row. For each group of 8 codebooks the 32 split values
 // are loaded (streaming, evict-first: each is used once), Algorithm 1 runs on
@@ -212,6 +213,11 @@ static bool cm_simple() {
   static int v = [] { const char* e = getenv("MDN_CM_SIMPLE"); return e ? atoi(e) : 0; }();
   return v != 0;
 }
+// MDN_CM_WS_ENCODE=0 keeps mdn_encode_cm on the thread-per-row kernel (A/B).
+static bool cm_ws_encode() {
+  static int v = [] { const char* e = getenv("MDN_CM_WS_ENCODE"); return e ? atoi(e) : 1; }();
+  return v != 0;
+}
 
 cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
                           int64_t ldt, float* out, int64_t ldo, cudaStream_t s) {
@@ -244,8 +250,11 @@ cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, 
 
 cudaError_t launch_encode_cm(const TreesDev& t, const float* At, int64_t N, int64_t ldt,
                              uint8_t* codes, cudaStream_t s) {
-  // Encode only: the thread-per-row kernel (measured 0.86-0.88 of HBM on
-  // 4 |S| + C/2 bytes per row; the TMA column-box variant reached 0.38).
+  if (!cm_simple() && cm_ws_encode()) {
+    bool done = false;
+    cudaError_t e = launch_encode_ws_cm(t, At, N, ldt, codes, s, &done);
+    if (done) return e;
+  }
   CmParams p{};
   p.At = At;
   p.N = N;

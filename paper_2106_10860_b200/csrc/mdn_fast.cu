@@ -83,7 +83,8 @@ struct Params {
   const float* thr;               // global [C][16]
   const uint16_t* q;              // global [C][16] 8-bit split values ceil(v) (uint8 input)
   const uint16_t* slot;           // column-major A: global [D] stage slot of each split column
-  const uint16_t* cols;           // column-major A: global [nslab] split column of each slot
+  const uint16_t* cols;           // column-major A: global [n_cols] split column of each slot
+  int n_cols;                     // column-major A: distinct split columns (nslab = n_cols rounded up to 4)
   float* out;
   uint8_t* codes;                 // encode-only output
 };
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
       s_off[si] = SUBF ? d - p.sub[i / 4] : (d / p.SW) * p.slab_e + (d % p.SW);
   }
   if constexpr (SUBF == CM)
-    for (int k = tid; k < p.nslab; k += blockDim.x) s_cols[k] = p.cols[k];
+    for (int k = tid; k < p.nslab; k += blockDim.x) s_cols[k] = p.cols[k < p.n_cols ? k : p.n_cols - 1];
   for (int c = tid; c < C; c += blockDim.x) {
     const int b = p.sub[c];
     s_base[c] = (b / p.SW) * p.slab_e + (b % p.SW);
@@ -284,10 +285,13 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
           if (lane == 0) mbar_arrive_tx(&full[s], bytes);
           TIn* dst = s_stage + (size_t)s * stage_e;
           if constexpr (SUBF == CM) {
-            // column-major A: one {R rows x 1 column} box per split column
+            // column-major A: TMA gather4 -- one instruction fetches R rows of
+            // 4 split columns (4 rows of At) into 4 consecutive slots; the
+            // slot count is padded to a multiple of 4 with the last column.
             __syncwarp();            // expect_tx before any complete_tx of this phase
-            for (int k = lane; k < p.nslab; k += 32)
-              tma_load_2d(dst + k * p.slab_e, &tmap, (int)y, s_cols[k], &full[s], p.l2_hint, pol);
+            for (int k = 4 * lane; k < p.nslab; k += 128)
+              tma_gather4(dst + k * p.slab_e, &tmap, (int)y, s_cols[k], s_cols[k + 1], s_cols[k + 2],
+                          s_cols[k + 3], &full[s]);
           } else {
             for (int k = 0; k < p.nslab; ++k)
               tma_load_2d(dst + k * p.slab_e, &tmap, k * p.SW, (int)y, &full[s], p.l2_hint, pol);
@@ -696,7 +700,7 @@ static cudaError_t encode_fast(const TreesDev& t, const TIn* A, int64_t N, int64
 static Geometry plan_cm(int C, int W, int n_cols, bool enc_only) {
   Geometry g;
   if (n_cols < 1 || n_cols > 4 * C) return g;
-  g.nslab = n_cols;
+  g.nslab = (n_cols + 3) & ~3;                     // gather4 fills slots in fours
   g.SW = 1;
   g.pad_e = 0;
   const int CBW = C >= 8 ? C / 8 : 1;
@@ -711,7 +715,7 @@ static Geometry plan_cm(int C, int W, int n_cols, bool enc_only) {
   for (int min_ns : {2}) {
     for (int R : {256, 128, 64, 32}) {
       if (force_r && R != force_r) continue;
-      const size_t stage = (size_t)n_cols * R * 4;
+      const size_t stage = (size_t)g.nslab * R * 4;
       if (fixed + stage * min_ns > budget) continue;
       int NS = (int)((budget - fixed) / stage);
       if (NS > NS_MAX) NS = NS_MAX;
@@ -746,10 +750,12 @@ static bool cm_ok(const TreesDev& t, const float* At, int64_t N, int64_t ldt) {
 cudaError_t launch_amm_ws_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
                              int64_t ldt, float* out, int64_t ldo, cudaStream_t s, bool* done) {
   *done = false;
-  // Only for heavy scans (W >= 8 table words per code, e.g. M = 100): with
-  // light scans the thread-per-row kernel of mdn_colmajor.cu, whose warps read
-  // the split columns directly, is as fast or faster (scale: 5.5 vs 4.8e9).
-  if (l.W < 8 || !cm_ok(t, At, N, ldt) || !has_combo(t.C, l.W, l.U)) return cudaSuccess;
+  // With TMA gather4 (4 split columns per box) this beats the thread-per-row
+  // kernel of mdn_colmajor.cu from 16 codebooks up (scale 8.5 vs 5.5e9,
+  // cls10_c16 1.97e10 vs 1.17e10, cls100 3.57 vs 2.56e9 rows/s); with 4-8
+  // codebooks of 32-value rows the thread-per-row kernel is faster (tiny 7.2
+  // vs 6.6e10, image 4.6 vs 4.2e10).
+  if (t.C < 16 || !cm_ok(t, At, N, ldt) || !has_combo(t.C, l.W, l.U)) return cudaSuccess;
   Geometry g = plan_cm(t.C, l.W, t.n_cols, false);
   if (!g.ok) return cudaSuccess;
   CUtensorMap tm;
@@ -757,6 +763,7 @@ cudaError_t launch_amm_ws_cm(const TreesDev& t, const LutsDev& l, const float* A
   Params p = base_params(t, g, N);
   p.slot = t.slot;
   p.cols = t.cols;
+  p.n_cols = t.n_cols;
   p.ldo = ldo;
   p.M = l.M;
   p.pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
@@ -767,11 +774,36 @@ cudaError_t launch_amm_ws_cm(const TreesDev& t, const LutsDev& l, const float* A
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
   *done = true;
 #define X(c, w, u)                                                                   \
-  if (t.C == c && l.W == w && l.U == u)                                              \
-    return vec ? launch_ws_sf<float, c, w, u, true, false, CM>(tm, p, g.smem, s)     \
-               : launch_ws_sf<float, c, w, u, false, false, CM>(tm, p, g.smem, s);
+  if constexpr (c >= 16)                                                             \
+    if (t.C == c && l.W == w && l.U == u)                                            \
+      return vec ? launch_ws_sf<float, c, w, u, true, false, CM>(tm, p, g.smem, s)   \
+                 : launch_ws_sf<float, c, w, u, false, false, CM>(tm, p, g.smem, s);
   MDN_FAST_COMBOS(X)
 #undef X
+  *done = false;
+  return cudaSuccess;
+}
+
+cudaError_t launch_encode_ws_cm(const TreesDev& t, const float* At, int64_t N, int64_t ldt,
+                                uint8_t* codes, cudaStream_t s, bool* done) {
+  *done = false;
+  if (t.C < 16 || !cm_ok(t, At, N, ldt) || !has_encoder(t.C)) return cudaSuccess;
+  if (reinterpret_cast<uintptr_t>(codes) & 3u) return cudaSuccess;
+  Geometry g = plan_cm(t.C, 1, t.n_cols, true);
+  if (!g.ok) return cudaSuccess;
+  CUtensorMap tm;
+  if (!make_tmap_cm(&tm, At, N, ldt, t.D, g.R)) return cudaSuccess;
+  Params p = base_params(t, g, N);
+  p.slot = t.slot;
+  p.cols = t.cols;
+  p.n_cols = t.n_cols;
+  p.codes = codes;
+  *done = true;
+  switch (t.C) {
+    case 16: return launch_ws_sf<float, 16, 1, 0, false, true, CM>(tm, p, g.smem, s);
+    case 32: return launch_ws_sf<float, 32, 1, 0, false, true, CM>(tm, p, g.smem, s);
+    case 64: return launch_ws_sf<float, 64, 1, 0, false, true, CM>(tm, p, g.smem, s);
+  }
   *done = false;
   return cudaSuccess;
 }

@@ -74,11 +74,13 @@ cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, 
                           int64_t ldt, float* out, int64_t ldo, cudaStream_t s);
 cudaError_t launch_encode_cm(const TreesDev& t, const float* At, int64_t N, int64_t ldt,
                              uint8_t* codes, cudaStream_t s);
-// Warp-specialised TMA variant of the fused path for column-major A with heavy
-// scans (mdn_fast.cu); *done = false when not applicable (the caller then uses
+// Warp-specialised TMA-gather4 variant of the fused path for column-major A
+// (mdn_fast.cu); *done = false when not applicable (the caller then uses
 // mdn_colmajor.cu's thread-per-row kernel).
 cudaError_t launch_amm_ws_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
                              int64_t ldt, float* out, int64_t ldo, cudaStream_t s, bool* done);
+cudaError_t launch_encode_ws_cm(const TreesDev& t, const float* At, int64_t N, int64_t ldt,
+                                uint8_t* codes, cudaStream_t s, bool* done);
 const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A, int64_t lda,
                              const float* out, int64_t ldo);
 

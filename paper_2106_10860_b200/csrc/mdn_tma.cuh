@@ -73,6 +73,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
   }
 }
 
+// TMA gather4 (sm_100a): rows r0..r3 of a 2-D tensor, `box inner` elements
+// each from column x, land back to back at dst (box height 1 in the map).
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int x, int r0, int r1,
+                                            int r2, int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(su32(bar))
+      : "memory");
+}
+
 // Host helpers (mdn_fast.cu).
 struct DevInfo {
   int sms = 148;
