@@ -48,18 +48,21 @@ def _dist():
 
 
 def _clock_sampler(device_index):
-    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     try:
         return subprocess.Popen(["nvidia-smi", f"--id={device_index}", f"--query-gpu={q}",
-                                 "--format=csv,noheader,nounits", "-lms", "100"],
+                                 "--format=csv,noheader,nounits", "-lms", "20"],
                                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
     except Exception:
         return None
 
 
-def _clock_summary(proc):
+def _clock_summary(proc, t0=None, t1=None):
+    """Median SM clock and the throttle reasons seen while the timed region
+    ran (samples stamped between host times t0 and t1; all samples if none
+    fall inside, e.g. a region shorter than the sampling period)."""
     if proc is None:
         return None
     proc.terminate()
@@ -67,24 +70,29 @@ def _clock_summary(proc):
         out, _ = proc.communicate(timeout=5)
     except Exception:
         return None
-    sm, mx, reasons = [], 0.0, set()
+    import datetime
     names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    recs = []
     for line in out.strip().splitlines():
         f = [x.strip() for x in line.split(",")]
         if len(f) < 9:
             continue
         try:
-            sm.append(float(f[1]))
-            mx = max(mx, float(f[2]))
+            ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            ts = None
+        try:
+            recs.append((ts, float(f[1]), float(f[2]),
+                         {n for n, v in zip(names, f[5:9]) if v.lower().startswith("active")}))
         except ValueError:
             continue
-        for n, v in zip(names, f[5:9]):
-            if v.lower().startswith("active"):
-                reasons.add(n)
-    if not sm:
+    if not recs:
         return None
-    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-            "samples": len(sm)}
+    inside = [r for r in recs if r[0] is not None and t0 is not None and t0 <= r[0] <= t1]
+    use = inside or recs
+    return {"sm_mhz": statistics.median(r[1] for r in use), "sm_max_mhz": max(r[2] for r in recs),
+            "reasons": sorted(set().union(*(r[3] for r in use))), "samples": len(use),
+            "samples_in_timed_region": len(inside)}
 
 
 ORACLE_CHUNK = 16384
@@ -383,16 +391,18 @@ def run(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    t_wall0 = time.time()
     ev[0].record(stream)
     for i in range(args.steps):
         step()
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
+    t_wall1 = time.time()
     if ws > 1:
         dist.barrier()
     per_launch = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     elapsed_ms = ev[0].elapsed_time(ev[-1])
-    clocks = _clock_summary(clk)
+    clocks = _clock_summary(clk, t_wall0, t_wall1)
     elapsed_ms = allreduce_max(elapsed_ms)
 
     rows_total = n * ws * args.steps
@@ -569,7 +579,7 @@ def run(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--mode", choices=["exact", "avg"], default="exact")
     ap.add_argument("--config", default=CONFIG,
