@@ -205,7 +205,8 @@ int mdn_encode_pq(const mdn_model* model, const float* A, int64_t N, int64_t lda
  * run through the fused kernel and copied back, with the copies of one chunk
  * overlapping the kernel of another (`n_slots` device staging slots of
  * `chunk_rows` rows, one stream each). Owns its device staging buffers and
- * streams. For overlap the host buffers should be page-locked. */
+ * streams; `model` and `luts` are borrowed and must outlive the executor.
+ * For overlap the host buffers should be page-locked. */
 int mdn_exec_create(const mdn_model* model, const mdn_luts* luts, int64_t chunk_rows,
                     int n_slots, mdn_exec** out);
 void mdn_exec_free(mdn_exec* exec);
