@@ -53,7 +53,7 @@ constexpr int NS_MAX = 8;
 
 struct SParams {
   int64_t N, n_tiles, ldo;
-  int pitch_e;                   // elements per shared row (D + 16 bytes of padding)
+  int pitch_e;                   // elements per shared row (fp32: D + 4; 8-bit: D)
   int stage_b;                   // bytes per stage, 128-aligned
   int NS;
   int M;
@@ -168,7 +168,11 @@ __device__ __forceinline__ float u16_to_f(uint32_t s) {
 template <class TIn, int D, int C, int W2, int U, int VEC, bool BQ>
 __global__ void __launch_bounds__(THREADS, 1)
     k_amm_rt(const __grid_constant__ CUtensorMap tmap, const SParams p) {
-  constexpr int PITCH = D + 16 / (int)sizeof(TIn);  // shared row pitch (elements)
+  // Shared row pitch (elements): fp32 rows D + 4 (pitch == 4 mod 32 words);
+  // 8-bit rows D bytes unpadded, so the encoder's 4-row x 8-codebook word
+  // loads hit 32 distinct banks (a 48-byte pitch made them 2-way conflicted)
+  // and the stage holds a third fewer bytes.
+  constexpr int PITCH = sizeof(TIn) == 1 ? D : D + 16 / (int)sizeof(TIn);
   constexpr int RPW = 32 / C;                       // rows per encode iteration
   constexpr int CS = CodeStride<C>::value;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -418,7 +422,7 @@ static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int
   constexpr int es = sizeof(TIn);
   *done = false;
   if (N > (int64_t)0x7FFFFF00 || !rt_ok(t, l, A, lda, es)) return cudaSuccess;
-  const int pitch_e = t.D + 16 / es;
+  const int pitch_e = es == 1 ? t.D : t.D + 16 / es;     // must match the kernel's PITCH
   const int stage_b = ((R * pitch_e * es) + 127) & ~127;
   const int W2 = (l.M + 1) / 2;
   const size_t fixed = ((256 + (size_t)t.C * 16 * W2 * 4 + (size_t)NWK * 32 * (t.C == 8 ? 12 : 4) * 4) + 127) & ~size_t(127);
@@ -431,7 +435,9 @@ static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int
   // still incomplete, which the parity wait cannot tell apart.
   NS -= NS % NG;
   CUtensorMap tm;
-  if (!make_tmap(&tm, A, N, lda, t.D, t.D, R, es)) return cudaSuccess;
+  // box inner = SW + 16/es elements (make_tmap's padded box); SW = D - 16 for
+  // 8-bit rows gives the unpadded D-byte box
+  if (!make_tmap(&tm, A, N, lda, t.D, es == 1 ? t.D - 16 : t.D, R, es)) return cudaSuccess;
   SParams p{};
   p.N = N;
   p.n_tiles = (N + R - 1) / R;
