@@ -315,7 +315,11 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
           // 32 / NG rows, so their split columns differ and the per-row reads
           // (pitch == 4 mod 32 words) spread over more banks than 32 rows of
           // one column would (4-way conflicts: +47% shared wavefronts on scale).
-          const int g = NG > 1 ? u % NG : 0, r = NG > 1 ? u / NG : u;
+          // (Column-major stages are [slot][row]: there rows-fastest lanes read
+          // 32 consecutive words of one slot, conflict-free, while groups-fastest
+          // lanes would put 4 slots' rows on the same banks.)
+          constexpr bool ROWS_FAST = SUBF == CM || NG == 1;
+          const int g = ROWS_FAST ? u / p.R : u % NG, r = ROWS_FAST ? u % p.R : u / NG;
           const uint32_t word = encode_group<TIn, C, SUBF>(stg + r * pitch, s_off, s_base, s_thr, g * G);
           const int row_local = st * p.R + r;
           if constexpr (ENC_ONLY) {
