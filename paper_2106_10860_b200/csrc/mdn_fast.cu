@@ -58,9 +58,12 @@ __host__ __device__ constexpr int off_base(int c) { return 4 * c + 4 * (c >> 3);
 // codebook (W table words of 4 columns), so the encoder:scanner split follows
 // 25 : 4W -- 2:8 for the 100-column tables, 6:4 for 10-16 columns, 8:2 for
 // <= 8 columns (ncu on the image config: scanners idle 63% at 2:8).
-template <int W, bool ENC_ONLY>
+template <int W, bool ENC_ONLY, bool CMV = false>
 struct Roles {
-  static constexpr int E = ENC_ONLY ? 8 : (W >= 8 ? 2 : (W >= 3 ? 6 : 8));
+  // Column-major A with wide tables runs ~35% more rows/s than row-major
+  // (fewer bytes per row), so it gets 6 encoder warps instead of 2 (cls100:
+  // 3.65 -> 4.11e9 rows/s; 2 encoder warps could not keep up).
+  static constexpr int E = ENC_ONLY ? 8 : (W >= 8 ? (CMV ? 6 : 2) : (W >= 3 ? 6 : 8));
   static constexpr int S = ENC_ONLY ? 0 : (W >= 8 ? 8 : (W >= 3 ? 4 : 2));
   static constexpr int THREADS = 32 * (1 + E + S);
   static constexpr int ROWS_PER_SCANNER = ENC_ONLY ? 0 : BR / (32 * S);
@@ -187,14 +190,14 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
 }
 
 template <class TIn, int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF>
-__global__ void __launch_bounds__(Roles<W, ENC_ONLY>::THREADS, 1)
+__global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
     k_amm_ws(const __grid_constant__ CUtensorMap tmap, const Params p) {
   constexpr int G = C >= 8 ? 8 : C;      // codebooks per encoder unit (one code word)
   constexpr int NG = C / G;
   constexpr int CBW = NG;                // code words per row
-  constexpr int EW = Roles<W, ENC_ONLY>::E;
-  constexpr int SWN = Roles<W, ENC_ONLY>::S;
-  constexpr int KR = Roles<W, ENC_ONLY>::ROWS_PER_SCANNER;
+  constexpr int EW = Roles<W, ENC_ONLY, SUBF == CM>::E;
+  constexpr int SWN = Roles<W, ENC_ONLY, SUBF == CM>::S;
+  constexpr int KR = Roles<W, ENC_ONLY, SUBF == CM>::ROWS_PER_SCANNER;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NS_MAX;
@@ -531,7 +534,7 @@ cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cu
   cudaError_t attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr_err != cudaSuccess) return attr_err;
   int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
-  k<<<(unsigned)grid, Roles<W, ENC>::THREADS, smem, s>>>(tm, p);
+  k<<<(unsigned)grid, Roles<W, ENC, SUBF == CM>::THREADS, smem, s>>>(tm, p);
   return cudaGetLastError();
 }
 
