@@ -172,7 +172,7 @@ template <int C, int W, int U, bool VEC, bool ENC>
 cudaError_t launch(const CmParams& p, cudaStream_t s) {
   auto k = k_amm_cm<C, W, U, VEC, ENC>;
   const size_t smem = 16 * C * 4 + 4 * C * 8 + (ENC ? 0 : (size_t)C * W * 16 * 4);
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem);

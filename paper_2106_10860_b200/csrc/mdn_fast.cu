@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "mdn_internal.h"
@@ -416,6 +417,25 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+cudaError_t ensure_smem(const void* kernel, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = done.find({kernel, dev});
+    if (it != done.end() && it->second >= smem) return cudaSuccess;
+  }
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(mu);
+    size_t& v = done[{kernel, dev}];
+    if (smem > v) v = smem;
+  }
+  return e;
+}
+
 DevInfo dev_info() {
   static DevInfo cache[16];
   static bool have[16] = {};
@@ -530,8 +550,7 @@ bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int
 template <class TIn, int C, int W, int U, bool VEC, bool ENC, int SUBF>
 cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
   auto k = k_amm_ws<TIn, C, W, U, VEC, ENC, SUBF>;
-  // Per launch: the attribute is per device context and costs ~1 us.
-  cudaError_t attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (attr_err != cudaSuccess) return attr_err;
   int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
   k<<<(unsigned)grid, Roles<W, ENC, SUBF == CM>::THREADS, smem, s>>>(tm, p);
@@ -554,7 +573,7 @@ cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int
                           float* out, int64_t ldo, cudaStream_t s) {
   auto k = k_scan_fast<C, W, U, VEC>;
   size_t smem = (size_t)C * W * 16 * 4;
-  cudaError_t attr_err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (attr_err != cudaSuccess) return attr_err;
   int64_t blocks = (N + 255) / 256;
   int64_t cap = (int64_t)dev_info().sms * (smem > 100000 ? 1 : smem > 60000 ? 2 : 4);

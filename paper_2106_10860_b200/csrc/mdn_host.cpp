@@ -93,6 +93,27 @@ int dalloc(T** p, size_t count) {
 
 bool is_pow2(int u) { return u >= 1 && (u & (u - 1)) == 0; }
 
+// The fast kernels address rows with 32-bit TMA coordinates; larger calls
+// run as consecutive 2^30-row launches on the same stream (an 8-bit A of
+// 2^31 rows x 32 bytes fits a 180 GB B200).
+// MDN_ROW_CHUNK (a multiple of 256) overrides the chunk for tests.
+int64_t row_chunk() {
+  static const int64_t v = [] {
+    const char* e = getenv("MDN_ROW_CHUNK");
+    const int64_t c = e ? atoll(e) : 0;
+    return c >= 256 && c % 256 == 0 && c <= (int64_t(1) << 30) ? c : int64_t(1) << 30;
+  }();
+  return v;
+}
+
+template <class F>
+cudaError_t for_row_chunks(int64_t N, F&& launch) {
+  const int64_t ch = row_chunk();
+  cudaError_t e = cudaSuccess;
+  for (int64_t r0 = 0; r0 < N && e == cudaSuccess; r0 += ch) e = launch(r0, N - r0 < ch ? N - r0 : ch);
+  return e;
+}
+
 int set_err(size_t* err_off, size_t off, int st) {
   if (err_off) *err_off = off;
   return st;
@@ -518,7 +539,10 @@ int mdn_encode(const mdn_model* m, const float* A, int64_t N, int64_t lda, uint8
   if (!A || !codes || lda < m->D) return MDN_EINVAL;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
-  return cuda_status(launch_encode(m->trees(), A, N, lda, codes, (cudaStream_t)stream));
+  const int64_t nb = (m->C + 1) / 2;
+  return cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    return launch_encode(m->trees(), A + r0 * lda, n, lda, codes + r0 * nb, (cudaStream_t)stream);
+  }));
 }
 
 int mdn_scan(const mdn_luts* l, const uint8_t* codes, int64_t N, int32_t* sums, float* out,
@@ -528,7 +552,11 @@ int mdn_scan(const mdn_luts* l, const uint8_t* codes, int64_t N, int32_t* sums, 
   if (!codes || (!sums && !out) || (out && ldo < l->M)) return MDN_EINVAL;
   DeviceGuard g(l->device);
   if (!g.ok) return MDN_ECUDA;
-  return cuda_status(launch_scan(l->dev(), codes, N, sums, out, ldo, (cudaStream_t)stream));
+  const int64_t nb = (l->C + 1) / 2;
+  return cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    return launch_scan(l->dev(), codes + r0 * nb, n, sums ? sums + r0 * l->M : nullptr,
+                       out ? out + r0 * ldo : nullptr, ldo, (cudaStream_t)stream);
+  }));
 }
 
 int mdn_amm(const mdn_model* m, const mdn_luts* l, const float* A, int64_t N, int64_t lda,
@@ -541,7 +569,10 @@ int mdn_amm(const mdn_model* m, const mdn_luts* l, const float* A, int64_t N, in
   if (!A || !out || lda < m->D || ldo < l->M) return MDN_EINVAL;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
-  return cuda_status(launch_amm(m->trees(), l->dev(), A, N, lda, out, ldo, (cudaStream_t)stream));
+  return cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    return launch_amm(m->trees(), l->dev(), A + r0 * lda, n, lda, out + r0 * ldo, ldo,
+                      (cudaStream_t)stream);
+  }));
 }
 
 int mdn_encode_u8(const mdn_model* m, const uint8_t* A, int64_t N, int64_t lda, uint8_t* codes,
@@ -552,7 +583,10 @@ int mdn_encode_u8(const mdn_model* m, const uint8_t* A, int64_t N, int64_t lda, 
   if (!A || !codes || lda < m->D) return MDN_EINVAL;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
-  return cuda_status(launch_encode_u8(m->trees(), A, N, lda, codes, (cudaStream_t)stream));
+  const int64_t nb = (m->C + 1) / 2;
+  return cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    return launch_encode_u8(m->trees(), A + r0 * lda, n, lda, codes + r0 * nb, (cudaStream_t)stream);
+  }));
 }
 
 int mdn_amm_u8(const mdn_model* m, const mdn_luts* l, const uint8_t* A, int64_t N, int64_t lda,
@@ -565,8 +599,10 @@ int mdn_amm_u8(const mdn_model* m, const mdn_luts* l, const uint8_t* A, int64_t 
   if (!A || !out || lda < m->D || ldo < l->M) return MDN_EINVAL;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
-  return cuda_status(
-      launch_amm_u8(m->trees(), l->dev(), A, N, lda, out, ldo, (cudaStream_t)stream));
+  return cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    return launch_amm_u8(m->trees(), l->dev(), A + r0 * lda, n, lda, out + r0 * ldo, ldo,
+                         (cudaStream_t)stream);
+  }));
 }
 
 int mdn_encode_pq(const mdn_model* m, const float* A, int64_t N, int64_t lda, uint8_t* codes,
@@ -577,8 +613,11 @@ int mdn_encode_pq(const mdn_model* m, const float* A, int64_t N, int64_t lda, ui
   if (!A || !codes || lda < m->D) return MDN_EINVAL;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
-  return cuda_status(launch_encode_pq(m->trees(), m->d_P, m->d_sub, m->d_sub_e, A, N, lda, codes,
-                                      (cudaStream_t)stream));
+  const int64_t nb = (m->C + 1) / 2;
+  return cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    return launch_encode_pq(m->trees(), m->d_P, m->d_sub, m->d_sub_e, A + r0 * lda, n, lda,
+                            codes + r0 * nb, (cudaStream_t)stream);
+  }));
 }
 
 int mdn_encode_cm(const mdn_model* m, const float* At, int64_t N, int64_t ldt, uint8_t* codes,
@@ -589,7 +628,10 @@ int mdn_encode_cm(const mdn_model* m, const float* At, int64_t N, int64_t ldt, u
   if (!At || !codes || ldt < N) return MDN_EINVAL;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
-  return cuda_status(launch_encode_cm(m->trees(), At, N, ldt, codes, (cudaStream_t)stream));
+  const int64_t nb = (m->C + 1) / 2;
+  return cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    return launch_encode_cm(m->trees(), At + r0, n, ldt, codes + r0 * nb, (cudaStream_t)stream);
+  }));
 }
 
 int mdn_amm_cm(const mdn_model* m, const mdn_luts* l, const float* At, int64_t N, int64_t ldt,
@@ -602,8 +644,10 @@ int mdn_amm_cm(const mdn_model* m, const mdn_luts* l, const float* At, int64_t N
   if (!At || !out || ldt < N || ldo < l->M) return MDN_EINVAL;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
-  return cuda_status(
-      launch_amm_cm(m->trees(), l->dev(), At, N, ldt, out, ldo, (cudaStream_t)stream));
+  return cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    return launch_amm_cm(m->trees(), l->dev(), At + r0, n, ldt, out + r0 * ldo, ldo,
+                         (cudaStream_t)stream);
+  }));
 }
 
 int mdn_amm_variant(const mdn_model* m, const mdn_luts* l, int64_t lda, char* buf, size_t len) {

@@ -126,7 +126,7 @@ cudaError_t launch(const float* A, int64_t N, int64_t lda, int C, const float* c
                    uint8_t* codes, cudaStream_t s) {
   auto k = k_encode_pq<DS, R>;
   const size_t smem = (size_t)16 * DS * C * 4;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem);

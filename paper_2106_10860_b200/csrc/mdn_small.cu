@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 template <class TIn, int C, int W2, int U, int VEC, bool BQ>
 cudaError_t launch(const CUtensorMap& tm, const SParams& p, size_t smem, cudaStream_t st) {
   auto k = k_amm_rt<TIn, 32, C, W2, U, VEC, BQ>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   const int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
   k<<<(unsigned)grid, THREADS, smem, st>>>(tm, p);

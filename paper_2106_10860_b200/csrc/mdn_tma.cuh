@@ -90,6 +90,9 @@ struct DevInfo {
   int smem_optin = 232448;
 };
 DevInfo dev_info();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
+// size): the attribute costs ~1 us per call, more than a small launch.
+cudaError_t ensure_smem(const void* kernel, size_t smem);
 bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int SW, int R, int es);
 int knob_hint();
 bool knob_bq();

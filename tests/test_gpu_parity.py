@@ -205,3 +205,40 @@ def test_bench_size_sampled_parity(mdn, name, n_rows):
         del out
     del A
     torch.cuda.empty_cache()
+
+
+def test_row_chunking_subprocess():
+    """Calls above 2^30 rows run as consecutive chunk launches; MDN_ROW_CHUNK
+    shrinks the chunk so a 4099-row call crosses 4 chunk boundaries (run in a
+    subprocess: the library reads the knob once)."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle as O, paper_2106_10860_b200 as mdn
+from datagen.synth import make_config_data
+from helpers import model_bytes
+for name, C, M, U in (("cls10_c16", 16, 10, 16), ("tiny", 4, 4, 4)):
+    blob = model_bytes(name); om = O.read_model(blob)
+    _, A, B = make_config_data(name, n_test=4099)
+    A = A[:4099]
+    model = mdn.mdn_model_load(blob, 0)
+    luts = mdn.mdn_build_luts(model, B, 1, U)
+    codes_o, S_o, want = O.amm(A, om, O.make_luts(om, B, "avg", U))
+    dA = torch.from_numpy(A).cuda()
+    out = torch.empty((4099, M), device="cuda"); mdn.mdn_amm(model, luts, dA, out)
+    codes = torch.empty((4099, (C + 1) // 2), dtype=torch.uint8, device="cuda"); mdn.mdn_encode(model, dA, codes)
+    sums = torch.empty((4099, M), dtype=torch.int32, device="cuda"); mdn.mdn_scan(luts, codes, sums=sums)
+    outc = torch.empty((4099, M), device="cuda"); mdn.mdn_amm_cm(model, luts, dA.t().contiguous(), outc)
+    assert (out.cpu().numpy().view(np.uint32) == want.view(np.uint32)).all(), name
+    assert (outc.cpu().numpy().view(np.uint32) == want.view(np.uint32)).all(), name
+    assert (codes.cpu().numpy() == O.pack_codes(codes_o)).all(), name
+    assert (sums.cpu().numpy() == S_o).all(), name
+print("chunked ok")
+'''
+    import os
+    env = dict(os.environ, MDN_ROW_CHUNK="1024")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env["PYTHONPATH"] = os.pathsep.join([root, os.path.join(root, "tests")])
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "chunked ok" in r.stdout, r.stdout + r.stderr
