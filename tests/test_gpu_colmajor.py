@@ -109,3 +109,32 @@ def test_cm_bench_size_sampled_parity(mdn):
         del out
     del At
     torch.cuda.empty_cache()
+
+
+def test_cm_slot_padding_and_repeated_dims(mdn):
+    """The gather4 producer pads the split-column slots to a multiple of 4 with
+    the last column: a model whose distinct split columns are not a multiple
+    of 4 (repeated split dims, reading R3) must still match the oracle."""
+    import copy
+    from test_gpu_shapes import _model
+    om0, _, A = _model(16, 64)
+    om = copy.deepcopy(om0)                    # the cached model is shared with other tests
+    om.dims[0] = om.dims[0, 0]                 # codebook 0: one dim at every level
+    om.dims[1, 2] = om.dims[1, 0]
+    n_cols = len(set(om.dims.reshape(-1).tolist()))
+    if n_cols % 4 == 0:                        # make the count odd for certain
+        om.dims[2, 3] = om.dims[2, 0]
+        n_cols = len(set(om.dims.reshape(-1).tolist()))
+    assert n_cols % 4 != 0
+    blob = O.write_model(om)
+    B = np.random.default_rng(5).standard_normal((64, 12)).astype(np.float32)
+    model = mdn.mdn_model_load(blob, 0)
+    for mode, mi in (("exact", 0), ("avg", 1)):
+        luts = mdn.mdn_build_luts(model, B, mi, 16)
+        codes_o, _, want = O.amm(A, om, O.make_luts(om, B, mode, 16))
+        out = torch.full((A.shape[0], 12), float("nan"), device="cuda")
+        mdn.mdn_amm_cm(model, luts, _At(A), out)
+        _assert_out(out.cpu().numpy(), want)
+    codes = torch.empty((A.shape[0], 8), dtype=torch.uint8, device="cuda")
+    mdn.mdn_encode_cm(model, _At(A), codes)
+    assert (codes.cpu().numpy() == O.pack_codes(codes_o)).all()
