@@ -481,26 +481,27 @@ def run(args):
 
     # --- e2e: the same metric through the public API with HOST buffers --------
     e2e = None
-    if op == "amm" and not u8 and not col and not pq and (rank == 0 or ws > 1):
+    if op == "amm" and not col and not pq and (rank == 0 or ws > 1):
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
                                  n_slots=3)
-        n_e2e = min(n, (1 << 30) // (4 * spec.D))     # <= 1 GiB of pinned host A per rank
+        host_fn = mdn.mdn_amm_host_u8 if u8 else mdn.mdn_amm_host
+        n_e2e = min(n, (1 << 30) // (ea * spec.D))    # <= 1 GiB of pinned host A per rank
         A_h = A[:n_e2e].cpu().pin_memory()
         out_h = torch.empty((n_e2e, spec.M), dtype=torch.float32).pin_memory()
-        mdn.mdn_amm_host(ex, A_h, out_h)                      # warm-up
+        host_fn(ex, A_h, out_h)                               # warm-up
         e2e_steps = max(1, min(args.steps, 3))
         if ws > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            mdn.mdn_amm_host(ex, A_h, out_h)                  # synchronous: H2D + kernel + D2H
+            host_fn(ex, A_h, out_h)                           # synchronous: H2D + kernel + D2H
         t_e2e = allreduce_max(time.perf_counter() - t0)
         e2e = {"value": n_e2e * ws * e2e_steps / t_e2e, "unit": "rows/s",
                "rows_per_step": n_e2e * ws,
-               "h2d_bytes_per_step": n_e2e * 4 * spec.D * ws,
+               "h2d_bytes_per_step": n_e2e * ea * spec.D * ws,
                "d2h_bytes_per_step": n_e2e * 4 * spec.M * ws,
-               "steps": e2e_steps, "path": "mdn_amm_host (pinned host A -> 3-slot pipelined "
-               "H2D/kernel/D2H)"}
+               "steps": e2e_steps, "path": ("mdn_amm_host_u8" if u8 else "mdn_amm_host")
+               + " (pinned host A -> 3-slot pipelined H2D/kernel/D2H)"}
         ex.close()
         del A_h, out_h
 

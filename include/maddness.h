@@ -214,6 +214,10 @@ void mdn_exec_free(mdn_exec* exec);
  * when out_host holds every row. */
 int mdn_amm_host(mdn_exec* exec, const float* A_host, int64_t N, int64_t lda,
                  float* out_host, int64_t ldo);
+/* The same pipeline for natively 8-bit rows (mdn_amm_u8): A_host
+ * u8 N x D (lda bytes) -- a quarter of the host->device bytes per row. */
+int mdn_amm_host_u8(mdn_exec* exec, const uint8_t* A_host, int64_t N, int64_t lda,
+                    float* out_host, int64_t ldo);
 
 /* --------------------------------------------------------- diagnostics -- */
 

@@ -58,6 +58,7 @@ _SIGS = {
     "mdn_encode_cm": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "mdn_amm_cm": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "mdn_encode_pq": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
+    "mdn_amm_host_u8": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64]),
     "mdn_train": (_i32, [_vp, _i64, _i64, _i32, _i32, ct.c_double, _i32, _vp, ct.POINTER(_sz)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -335,6 +336,26 @@ def mdn_amm_host(ex: Exec, A_host, out_host):
     if so[0] != sa[0]:
         raise ValueError("row count mismatch")
     _check(_lib.mdn_amm_host(ex._h, pa, sa[0], lda, po, ldo), "mdn_amm_host")
+    return out_host
+
+
+def mdn_amm_host_u8(ex: Exec, A_host, out_host):
+    """Host-buffer pipeline for 8-bit rows: A_host uint8 (numpy or
+    CPU tensor, unit column stride), out_host float32."""
+    import torch
+    if isinstance(A_host, np.ndarray):
+        if A_host.dtype != np.uint8 or A_host.ndim != 2 or A_host.strides[1] != 1:
+            raise TypeError("A_host must be a 2-D uint8 array with unit column stride")
+        pa, lda, sa = A_host.ctypes.data, A_host.strides[0], A_host.shape
+    elif isinstance(A_host, torch.Tensor) and not A_host.is_cuda and A_host.dtype == torch.uint8 \
+            and A_host.dim() == 2 and A_host.stride(1) == 1:
+        pa, lda, sa = A_host.data_ptr(), A_host.stride(0), tuple(A_host.shape)
+    else:
+        raise TypeError("A_host must be host uint8 (numpy or CPU tensor)")
+    po, ldo, so = _host_ptr(out_host, "out_host")
+    if so[0] != sa[0]:
+        raise ValueError("row count mismatch")
+    _check(_lib.mdn_amm_host_u8(ex._h, pa, sa[0], lda, po, ldo), "mdn_amm_host_u8")
     return out_host
 
 

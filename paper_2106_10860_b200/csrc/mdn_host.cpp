@@ -728,7 +728,13 @@ int mdn_exec_create(const mdn_model* m, const mdn_luts* l, int64_t chunk_rows, i
   return MDN_OK;
 }
 
-int mdn_amm_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
+}  // extern "C"
+
+namespace {
+// Host-buffer pipeline shared by fp32 and 8-bit rows: chunk q goes H2D into
+// slot q % n_slots, through the fused kernel and back D2H on the slot's stream.
+template <class TIn>
+int amm_host(mdn_exec* x, const TIn* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
   if (!x || N < 0) return MDN_EINVAL;
   if (N == 0) return MDN_OK;
   const int D = x->model->D, M = x->luts->M;
@@ -741,20 +747,41 @@ int mdn_amm_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* out
     int s = (int)(q % x->n_slots);
     cudaStream_t st = x->streams[s];
     int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
+    TIn* dA = reinterpret_cast<TIn*>(x->dA[s]);        // sized for fp32 rows: 8-bit rows fit
     // Stream order serialises reuse of slot s: H2D(q) waits for D2H(q - n_slots).
-    e = cudaMemcpy2DAsync(x->dA[s], D * sizeof(float), A + r0 * lda, lda * sizeof(float),
-                          D * sizeof(float), n, cudaMemcpyHostToDevice, st);
+    // Contiguous rows go as one linear copy: a 2-D copy of narrow rows (8-bit
+    // A, small M) runs row by row and far below the PCIe rate.
+    e = lda == D ? cudaMemcpyAsync(dA, A + r0 * lda, (size_t)n * D * sizeof(TIn), cudaMemcpyHostToDevice, st)
+                 : cudaMemcpy2DAsync(dA, D * sizeof(TIn), A + r0 * lda, lda * sizeof(TIn), D * sizeof(TIn),
+                                     n, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) break;
-    e = launch_amm(x->model->trees(), x->luts->dev(), x->dA[s], n, D, x->dOut[s], M, st);
+    if constexpr (sizeof(TIn) == 1)
+      e = launch_amm_u8(x->model->trees(), x->luts->dev(), dA, n, D, x->dOut[s], M, st);
+    else
+      e = launch_amm(x->model->trees(), x->luts->dev(), dA, n, D, x->dOut[s], M, st);
     if (e != cudaSuccess) break;
-    e = cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
-                          M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
+    e = ldo == M ? cudaMemcpyAsync(out + r0 * ldo, x->dOut[s], (size_t)n * M * sizeof(float),
+                                   cudaMemcpyDeviceToHost, st)
+                 : cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
+                                     M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
   }
   for (auto s : x->streams) {
     cudaError_t e2 = cudaStreamSynchronize(s);
     if (e == cudaSuccess) e = e2;
   }
   return cuda_status(e);
+}
+}  // namespace
+
+extern "C" {
+
+int mdn_amm_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
+  return amm_host<float>(x, A, N, lda, out, ldo);
+}
+
+int mdn_amm_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, float* out,
+                    int64_t ldo) {
+  return amm_host<uint8_t>(x, A, N, lda, out, ldo);
 }
 
 }  // extern "C"

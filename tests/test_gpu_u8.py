@@ -77,3 +77,19 @@ def test_u8_generic_fallback_and_ragged(mdn):
         out = torch.empty((A.shape[0], 4), device="cuda")
         mdn.mdn_amm_u8(model, luts, view, out)
         assert (out.cpu().numpy().view(np.uint32) == want.view(np.uint32)).all()
+
+
+def test_u8_host_executor(mdn):
+    """mdn_amm_host_u8: pinned host 8-bit rows through the pipelined executor
+    (chunks smaller than N, so several slots cycle) equal the oracle."""
+    blob = model_bytes("image_u8")
+    om = O.read_model(blob)
+    _, A, B = make_config_data("image_u8", n_test=50_001, n_train=0)
+    model = mdn.mdn_model_load(blob, 0)
+    luts = mdn.mdn_build_luts(model, B, 1, 8)
+    want = O.amm_u8(A, om, O.make_luts(om, B, "avg", 8))[2]
+    ex = mdn.mdn_exec_create(model, luts, chunk_rows=4096, n_slots=3)
+    A_h = torch.from_numpy(A).pin_memory()
+    out_h = torch.empty((A.shape[0], 2)).pin_memory()
+    mdn.mdn_amm_host_u8(ex, A_h, out_h)
+    assert (out_h.numpy().view(np.uint32) == want.view(np.uint32)).all()
