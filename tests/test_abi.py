@@ -150,3 +150,26 @@ def test_bench_split_dims_parser():
     for name in ("tiny", "cls100", "scale"):
         blob = model_bytes(name)
         assert bench.split_dims(blob) == sorted(set(O.read_model(blob).dims.reshape(-1).tolist()))
+
+
+def test_null_handle_guards_every_hot_path_call(lib):
+    """Every device entry point rejects a NULL handle with MDN_EINVAL before
+    touching a device (widened rows N1-N4 included)."""
+    P, I = ct.c_void_p, ct.c_int64
+    calls = {
+        "mdn_encode_u8": ([P, P, I, I, P, P], (None, None, 1, 1, None, None)),
+        "mdn_amm_u8": ([P, P, P, I, I, P, I, P], (None, None, None, 1, 1, None, 1, None)),
+        "mdn_encode_cm": ([P, P, I, I, P, P], (None, None, 1, 1, None, None)),
+        "mdn_amm_cm": ([P, P, P, I, I, P, I, P], (None, None, None, 1, 1, None, 1, None)),
+        "mdn_encode_pq": ([P, P, I, I, P, P], (None, None, 1, 1, None, None)),
+        "mdn_scan": ([P, P, I, P, P, I, P], (None, None, 1, None, None, 1, None)),
+        "mdn_amm_host": ([P, P, I, I, P, I], (None, None, 1, 1, None, 1)),
+        "mdn_amm_host_u8": ([P, P, I, I, P, I], (None, None, 1, 1, None, 1)),
+    }
+    for name, (argtypes, args) in calls.items():
+        f = getattr(lib, name)
+        f.argtypes = argtypes
+        assert f(*args) == -1, name
+    # negative N is rejected too
+    lib.mdn_encode.argtypes = [P, P, I, I, P, P]
+    assert lib.mdn_encode(None, None, -1, 1, None, None) == -1
