@@ -450,7 +450,7 @@ def run(args):
         sm_mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
         fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
         tflops = n * 48 * spec.D / t_enc / 1e12
-        pq_roof = {"bound": "fp32", "achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+        pq_roof = {"bound": "alu", "achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s",
                    "frac": tflops / fp32_peak, "peak_kind": "derived: 148 SMs x 128 fp32 lanes x clock",
                    "traffic": None, "algorithmic_flops_per_launch": n * 48 * spec.D,
                    "kernel": "k_encode_pq", "encode_rows_per_s": n / t_enc}
