@@ -860,15 +860,25 @@ cudaError_t launch_amm_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A,
 
 cudaError_t launch_encode(const TreesDev& t, const float* A, int64_t N, int64_t lda, uint8_t* codes,
                           cudaStream_t s) {
-  bool done;
-  cudaError_t e = encode_fast<float>(t, A, N, lda, codes, s, &done);
+  bool done = false;
+  cudaError_t e;
+  if (rt_enabled()) {
+    e = launch_encode_rt(t, A, N, lda, codes, s, &done);
+    if (done) return e;
+  }
+  e = encode_fast<float>(t, A, N, lda, codes, s, &done);
   return done ? e : launch_encode_generic(t, A, 4, N, lda, codes, s);
 }
 
 cudaError_t launch_encode_u8(const TreesDev& t, const uint8_t* A, int64_t N, int64_t lda,
                              uint8_t* codes, cudaStream_t s) {
-  bool done;
-  cudaError_t e = encode_fast<uint8_t>(t, A, N, lda, codes, s, &done);
+  bool done = false;
+  cudaError_t e;
+  if (rt_enabled()) {
+    e = launch_encode_rt_u8(t, A, N, lda, codes, s, &done);
+    if (done) return e;
+  }
+  e = encode_fast<uint8_t>(t, A, N, lda, codes, s, &done);
   return done ? e : launch_encode_generic(t, A, 1, N, lda, codes, s);
 }
 

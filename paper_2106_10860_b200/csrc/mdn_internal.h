@@ -65,6 +65,10 @@ cudaError_t launch_amm_rt(const TreesDev& t, const LutsDev& l, const float* A, i
 cudaError_t launch_amm_rt_u8(const TreesDev& t, const LutsDev& l, const uint8_t* A, int64_t N,
                              int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done);
 bool amm_rt_applies(const TreesDev& t, const LutsDev& l, int es);
+cudaError_t launch_encode_rt(const TreesDev& t, const float* A, int64_t N, int64_t lda,
+                             uint8_t* codes, cudaStream_t s, bool* done);
+cudaError_t launch_encode_rt_u8(const TreesDev& t, const uint8_t* A, int64_t N, int64_t lda,
+                                uint8_t* codes, cudaStream_t s, bool* done);
 // PQ encoder (mdn_pq.cu).
 cudaError_t launch_encode_pq(const TreesDev& t, const float* P_dense, const uint16_t* sub_b,
                              const uint16_t* sub_e, const float* A, int64_t N, int64_t lda,

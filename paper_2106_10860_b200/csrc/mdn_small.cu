@@ -64,6 +64,7 @@ struct SParams {
   const float* thr;              // global [C][16]
   const uint16_t* q;             // global [C][16]
   float* out;
+  uint8_t* codes;                // encode-only: packed 4-bit codes, N x C/2
 };
 
 // Code rows are C words (one table address per codebook). C = 8: rows whose
@@ -134,14 +135,18 @@ __device__ __forceinline__ uint32_t push_sign(uint32_t n, uint32_t d) {
   return r;
 }
 
-template <int W2>
-__device__ __forceinline__ uint32_t byte_tree_addr(uint32_t w, const ByteTree& b) {
+// 15 - code (the complemented leaf index n_4) for 8-bit rows; see byte_tree_addr.
+__device__ __forceinline__ uint32_t byte_tree_n4(uint32_t w, const ByteTree& b) {
   const uint32_t lt0 = sign_bit(prmt(w, 0u, b.s0) - (uint32_t)b.q0);
   const uint32_t v1 = (uint32_t)b.q2 + lt0 * (uint32_t)b.d12;
   const uint32_t n2 = push_sign(lt0, prmt(w, 0u, b.s1) - v1);
   const uint32_t n3 = push_sign(n2, prmt(w, b.g2, b.s2) - prmt(b.Q2, b.Q2, n2));
-  const uint32_t n4 = push_sign(n3, prmt(w, b.g3, b.s3) - prmt(b.Q3lo, b.Q3hi, n3));   // 15 - code
-  return b.base - n4 * (4u * W2);
+  return push_sign(n3, prmt(w, b.g3, b.s3) - prmt(b.Q3lo, b.Q3hi, n3));
+}
+
+template <int W2>
+__device__ __forceinline__ uint32_t byte_tree_addr(uint32_t w, const ByteTree& b) {
+  return b.base - byte_tree_n4(w, b) * (4u * W2);   // 15 - n4 = code
 }
 
 // mu(a, b) = floor((a + b + 1) / 2) on two 16-bit lanes holding values < 256
@@ -165,7 +170,10 @@ __device__ __forceinline__ float u16_to_f(uint32_t s) {
 // 4-byte subspaces [4c, 4c + 4) (the image config; other byte layouts use the
 // general kernel). VEC: 0 = guarded scalar stores, 1 = M == 2 W2 with 8-byte
 // (W2 odd) or 16-byte (W2 even) aligned rows.
-template <class TIn, int D, int C, int W2, int U, int VEC, bool BQ>
+// ENC: encode only (mdn_encode / mdn_encode_u8): the C lanes of a row OR
+// their nibbles together with shuffles and one lane stores the row's packed
+// codes; no tables, no scan.
+template <class TIn, int D, int C, int W2, int U, int VEC, bool BQ, bool ENC = false>
 __global__ void __launch_bounds__(THREADS, 1)
     k_amm_rt(const __grid_constant__ CUtensorMap tmap, const SParams p) {
   // Shared row pitch (elements): fp32 rows D + 4 (pitch == 4 mod 32 words);
@@ -180,12 +188,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* empty = full + NS_MAX;
   constexpr int OFF_LUT = 256;
   constexpr int OFF_CODE = OFF_LUT + C * 16 * W2 * 4;
-  constexpr int OFF_STAGE = (OFF_CODE + NWK * 32 * CS * 4 + 127) & ~127;
+  constexpr int OFF_STAGE = ENC ? 256 : (OFF_CODE + NWK * 32 * CS * 4 + 127) & ~127;
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
 
-  for (int i = tid; i < C * 16 * W2; i += blockDim.x) s_lut[i] = p.lut16[i];
+  if constexpr (!ENC)
+    for (int i = tid; i < C * 16 * W2; i += blockDim.x) s_lut[i] = p.lut16[i];
   if (tid == 0) {
     for (int s = 0; s < p.NS; ++s) {
       mbar_init(&full[s], 1);
@@ -266,6 +275,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     bt.s3 = j3 | 0x4440u;
     bt.base = lut_c + 15u * 4u * W2;
   }
+  // ENC transpose constants: stage k exchanges with lane c ^ 2^k; a lane whose
+  // bit k is b keeps the nibbles whose index has bit k == b and receives the
+  // partner's rotated by 4 * 2^k the other way.
+  constexpr int LOGC = C == 8 ? 3 : 2;
+  uint32_t t_rot[LOGC], t_sel[LOGC];
+#pragma unroll
+  for (int k = 0; k < LOGC; ++k) {
+    const uint32_t lo = k == 0 ? 0x0F0F0F0Fu : (k == 1 ? 0x00FF00FFu : 0x0000FFFFu);
+    const bool b = (c >> k) & 1;
+    t_rot[k] = b ? 32u - (4u << k) : (4u << k);
+    t_sel[k] = (b ? ~lo : lo) | (C == 4 ? 0xFFFF0000u : 0u);
+  }
   int s = grp, ph = 0;
   while (s >= p.NS) s -= p.NS, ph ^= 1;
   // This lane's output row and pointer, advanced by a constant stride per stage.
@@ -288,10 +309,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         w[it] = *reinterpret_cast<const uint32_t*>(stg + it * RPW * PITCH + sub);
 #pragma unroll
       for (int it = 0; it < C; ++it) {
-        if constexpr (BQ)
+        if constexpr (BQ && ENC)
+          code[it] = 15u - byte_tree_n4(w[it], bt);
+        else if constexpr (BQ)
           code[it] = byte_tree_addr<W2>(w[it], bt);
         else
-          code[it] = lut_c + 4u * W2 *
+          code[it] = (ENC ? 0u : lut_c) + (ENC ? 1u : 4u * W2) *
                      tree_code<int>((int)__byte_perm(w[it], 0u, sel[0]), (int)__byte_perm(w[it], 0u, sel[1]),
                                     (int)__byte_perm(w[it], 0u, sel[2]), (int)__byte_perm(w[it], 0u, sel[3]), th);
       }
@@ -303,7 +326,36 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int t = 0; t < 4; ++t) x[it][t] = stg[it * RPW * PITCH + o[t]];
 #pragma unroll
       for (int it = 0; it < C; ++it)
-        code[it] = lut_c + 4u * W2 * tree_code<float>(x[it][0], x[it][1], x[it][2], x[it][3], th);
+        code[it] = (ENC ? 0u : lut_c) + (ENC ? 1u : 4u * W2) *
+                   tree_code<float>(x[it][0], x[it][1], x[it][2], x[it][3], th);
+    }
+    if constexpr (ENC) {
+      // Lane (rs, c) holds codebook c of rows it * RPW + rs: a C x C nibble
+      // matrix over the group's lanes. Pack it (nibble it), then transpose it
+      // with log2(C) butterfly stages (rotate, shuffle, merge) so that lane
+      // (rs, c) holds row c * RPW + rs, and the warp's 32 rows leave in one
+      // coalesced store (low nibble = even codebook, L147 / L608).
+      uint32_t keep = code[C - 1];
+#pragma unroll
+      for (int it = C - 2; it >= 0; --it) keep = keep * 16u + code[it];
+#pragma unroll
+      for (int k = 0; k < LOGC; ++k) {
+        const uint32_t t = __funnelshift_r(keep, keep, t_rot[k]);
+        const uint32_t r = __shfl_xor_sync(0xffffffffu, t, 1 << k);
+        keep = (keep & t_sel[k]) | (r & ~t_sel[k]);
+      }
+      const int64_t r = ((int64_t)blockIdx.x + q * gridDim.x) * R + chunk * 32 + c * RPW + rs;
+      if (r < p.N) {
+        if constexpr (C == 8)
+          reinterpret_cast<uint32_t*>(p.codes)[r] = keep;
+        else
+          reinterpret_cast<uint16_t*>(p.codes)[r] = (uint16_t)keep;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      s += NG;
+      while (s >= p.NS) s -= p.NS, ph ^= 1;
+      continue;
     }
 #pragma unroll
     for (int it = 0; it < C; ++it) {
@@ -379,6 +431,16 @@ __global__ void __launch_bounds__(THREADS, 1)
 template <class TIn, int C, int W2, int U, int VEC, bool BQ>
 cudaError_t launch(const CUtensorMap& tm, const SParams& p, size_t smem, cudaStream_t st) {
   auto k = k_amm_rt<TIn, 32, C, W2, U, VEC, BQ>;
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
+  k<<<(unsigned)grid, THREADS, smem, st>>>(tm, p);
+  return cudaGetLastError();
+}
+
+template <class TIn, int C, bool BQ>
+cudaError_t launch_enc(const CUtensorMap& tm, const SParams& p, size_t smem, cudaStream_t st) {
+  auto k = k_amm_rt<TIn, 32, C, 1, 0, 0, BQ, true>;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   const int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
@@ -467,6 +529,56 @@ static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int
   if (t.C == 8 && W2 == 2) return avg ? launch_v<TIn, 8, 2, 8>(tm, p, smem, vec, bq, st) : launch_v<TIn, 8, 2, 0>(tm, p, smem, vec, bq, st);
   *done = false;
   return cudaSuccess;
+}
+
+// Encode-only variant: same pipeline, same trees, packed codes out.
+template <class TIn>
+static cudaError_t encode_rt(const TreesDev& t, const TIn* A, int64_t N, int64_t lda,
+                             uint8_t* codes, cudaStream_t st, bool* done) {
+  constexpr int es = sizeof(TIn);
+  *done = false;
+  if (N > (int64_t)0x7FFFFF00 || !(t.C == 4 || t.C == 8) || t.D != 32) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(A) & 15u) || (lda * es) % 16) return cudaSuccess;
+  if (es == 1 && t.subf_u8 != 1) return cudaSuccess;
+  if (reinterpret_cast<uintptr_t>(codes) & (uintptr_t)(t.C / 2 - 1)) return cudaSuccess;
+  const int pitch_e = es == 1 ? t.D : t.D + 16 / es;
+  const int stage_b = ((R * pitch_e * es) + 127) & ~127;
+  const size_t fixed = 256;                          // barriers only (kernel's OFF_STAGE)
+  const size_t budget = (size_t)dev_info().smem_optin;
+  int NS = (int)((budget - fixed) / stage_b);
+  if (NS > NS_MAX) NS = NS_MAX;
+  NS -= NS % NG;
+  if (NS < NG) return cudaSuccess;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, A, N, lda, t.D, es == 1 ? t.D - 16 : t.D, R, es)) return cudaSuccess;
+  SParams p{};
+  p.N = N;
+  p.n_tiles = (N + R - 1) / R;
+  p.pitch_e = pitch_e;
+  p.stage_b = stage_b;
+  p.NS = NS;
+  p.dims = t.dims;
+  p.sub = t.sub;
+  p.thr = t.thr;
+  p.q = t.q;
+  p.codes = codes;
+  const size_t smem = fixed + (size_t)NS * stage_b;
+  const bool bq = es == 1 && t.q_byte && knob_bq();
+  *done = true;
+  if constexpr (es == 1) {
+    if (bq) return t.C == 4 ? launch_enc<TIn, 4, true>(tm, p, smem, st) : launch_enc<TIn, 8, true>(tm, p, smem, st);
+  }
+  return t.C == 4 ? launch_enc<TIn, 4, false>(tm, p, smem, st) : launch_enc<TIn, 8, false>(tm, p, smem, st);
+}
+
+cudaError_t launch_encode_rt(const TreesDev& t, const float* A, int64_t N, int64_t lda,
+                             uint8_t* codes, cudaStream_t st, bool* done) {
+  return encode_rt<float>(t, A, N, lda, codes, st, done);
+}
+
+cudaError_t launch_encode_rt_u8(const TreesDev& t, const uint8_t* A, int64_t N, int64_t lda,
+                                uint8_t* codes, cudaStream_t st, bool* done) {
+  return encode_rt<uint8_t>(t, A, N, lda, codes, st, done);
 }
 
 cudaError_t launch_amm_rt(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,

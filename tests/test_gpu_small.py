@@ -141,3 +141,48 @@ def test_bench_size_sampled_parity(mdn, name):
         del out
     del A
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("C", [4, 8])
+@pytest.mark.parametrize("N", [1, 31, 255, 257, 4097, 70_001])
+def test_rt_encode_ragged(mdn, C, N):
+    """Encode-only register-tree kernel (mdn_encode, C in {4, 8}, D = 32): packed
+    codes bit-exact, strided A (lda = 36), nothing written past row N."""
+    om, blob, A = _model(C)
+    A = A[:N]
+    model = mdn.mdn_model_load(blob, 0)
+    big = torch.zeros((N, 36), device="cuda")
+    big[:, :32] = torch.from_numpy(A).cuda()
+    codes = torch.full((N + 3, C // 2), 0xAB, dtype=torch.uint8, device="cuda")
+    mdn.mdn_encode(model, big[:, :32], codes[:N])
+    got = codes.cpu().numpy()
+    assert (got[:N] == O.pack_codes(O.encode(A, om))).all()
+    assert (got[N:] == 0xAB).all()
+
+
+@pytest.mark.parametrize("q256", [False, True], ids=["byte_tree", "int_tree"])
+def test_rt_encode_u8(mdn, q256):
+    """mdn_encode_u8 through the register-tree encoder: byte-threshold trees and
+    (a split value of 256) the integer select tree."""
+    om = O.read_model(model_bytes("image_u8"))
+    if q256:
+        om.thr = om.thr.copy()
+        om.thr[5, 9] = np.float32(255.5)
+    A, _ = _u8_data()
+    model = mdn.mdn_model_load(O.write_model(om), 0)
+    for n in (A.shape[0], 257, 1):
+        codes = torch.empty((n, 4), dtype=torch.uint8, device="cuda")
+        mdn.mdn_encode_u8(model, torch.from_numpy(A[:n]).cuda(), codes)
+        assert (codes.cpu().numpy() == O.pack_codes(O.encode_u8(A[:n], om))).all()
+
+
+def test_rt_encode_unaligned_codes_falls_back(mdn):
+    """Codes at an odd byte offset (C = 8 wants 4-byte rows): the general
+    encoder takes over and still matches."""
+    om, blob, A = _model(8)
+    A = A[:1000]
+    model = mdn.mdn_model_load(blob, 0)
+    raw = torch.zeros(1000 * 4 + 1, dtype=torch.uint8, device="cuda")
+    codes = raw[1:].view(1000, 4)
+    mdn.mdn_encode(model, torch.from_numpy(A).cuda(), codes)
+    assert (codes.cpu().numpy() == O.pack_codes(O.encode(A, om))).all()
