@@ -434,7 +434,7 @@ def run(args):
     peak, peak_kind = _peaks()
     avg_launch_s = statistics.mean(per_launch) / 1e3
     achieved_gbs = n * bytes_per_row / avg_launch_s / 1e9
-    pq_roof = None
+    alu_roof = None
     if pq:
         # The PQ encoder is bound by the fp32 pipe, not HBM: 16 prototypes x D
         # dims x (subtract, multiply, add) per row (Eq. pqLoss, no FMA).
@@ -450,10 +450,24 @@ def run(args):
         sm_mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
         fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
         tflops = n * 48 * spec.D / t_enc / 1e12
-        pq_roof = {"bound": "alu", "achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+        alu_roof = {"bound": "alu", "achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s",
                    "frac": tflops / fp32_peak, "peak_kind": "derived: 148 SMs x 128 fp32 lanes x clock",
                    "traffic": None, "algorithmic_flops_per_launch": n * 48 * spec.D,
                    "kernel": "k_encode_pq", "encode_rows_per_s": n / t_enc}
+
+    if op == "scan" and not pq:
+        # Unfused mdn_scan moves (C/2 + 4M) B/row but does C*M table-byte
+        # lookups per row: it is bound by instruction issue, not HBM. SURVEY
+        # 8(d): report lookups/s against the issue ceiling (148 SMs x 128
+        # lanes x clock thread-instructions/s, derived).
+        sm_mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
+        issue_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+        lk = n * spec.C * spec.M / avg_launch_s / 1e12
+        alu_roof = {"bound": "alu", "achieved": lk, "peak": issue_peak,
+                   "unit": "T lookups/s vs T thread-instr/s", "frac": lk / issue_peak,
+                   "peak_kind": "derived: 148 SMs x 128 lanes x clock (issue ceiling)",
+                   "traffic": None, "algorithmic_lookups_per_launch": n * spec.C * spec.M,
+                   "kernel": "scan", "hbm_gbs": achieved_gbs}
 
     # --- quality (NMSE vs exact fp64 AB on 65536 rows) and the cuBLAS context point
     nmse = None
@@ -552,7 +566,7 @@ def run(args):
                        "l2": f"inputs {n * 4 * spec.D / 2**30:.1f} GiB per GPU > 126 MB L2; no flush",
                        "parallelism": f"row-sharded dp{ws}, model+LUT NCCL broadcast once"},
             "pct_hbm_nominal_8tbs": achieved_gbs / NOMINAL_HBM_GBS,
-            "roofline": pq_roof or {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+            "roofline": alu_roof or {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "peak_kind": peak_kind,
                          "traffic": traffic,
                          "algorithmic_bytes_per_launch": n * bytes_per_row,

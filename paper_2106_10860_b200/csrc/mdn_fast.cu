@@ -368,12 +368,12 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
 
 // ------------------------------------------------------------ scan kernel --
 
-template <int C, int W, int U, bool VEC>
+template <int C, int W, int U, bool VEC, int MIX>
 __global__ void __launch_bounds__(256) k_scan_fast(const uint32_t* __restrict__ lut_g,
                                                    const uint8_t* __restrict__ codes, int64_t N,
                                                    int M, int32_t* __restrict__ sums,
                                                    float* __restrict__ out, int64_t ldo, float a,
-                                                   float b, int scale) {
+                                                   float b, int scale, bool pair) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
   for (int i = threadIdx.x; i < C * W * 4; i += blockDim.x)
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256) k_scan_fast(const uint32_t* __restrict__ 
        row += (int64_t)gridDim.x * blockDim.x) {
     const uint8_t* cr = codes + row * ((C + 1) / 2);
     uint32_t ae[W], ao[W];
-    scan_core<C, W, U>(
+    scan_core<C, W, U, false, MIX>(
         s_lut,
         [&](int g) -> uint32_t {
           if constexpr (C >= 8) return __ldg(reinterpret_cast<const uint32_t*>(cr) + g);
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(256) k_scan_fast(const uint32_t* __restrict__ 
         },
         ae, ao);
     if (sums) store_sums<W>(sums + row * M, M, scale, ae, ao);
-    if (out) store_row<W, VEC>(out + row * ldo, M, ae, ao, a, b);
+    if (out) store_row<W, VEC>(out + row * ldo, M, ae, ao, a, b, pair);
   }
 }
 
@@ -568,18 +568,39 @@ cudaError_t launch_ws_t(const CUtensorMap& tm, const Params& p, int subf, size_t
   return launch_ws_sf<TIn, C, W, U, VEC, ENC, 0>(tm, p, smem, s);
 }
 
+// Exact-mode pipe mix of the standalone scan (mdn_scan.cuh). Measured (same
+// box, rows/s, mix vs ALU-only): cls100 +7%, scale +8%, cls10_c64 +8%,
+// cls10_c16 -6%, C <= 8 unchanged; so the default (-1) mixes for C >= 32.
+// MDN_SCAN_MIX=0 forces ALU-only, 3 forces the mix.
+static int scan_mix(int C) {
+  static const int v = env_int("MDN_SCAN_MIX", -1);
+  return v < 0 ? (C >= 32 ? 3 : 0) : v;
+}
+
 template <int C, int W, int U, bool VEC>
 cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int32_t* sums,
                           float* out, int64_t ldo, cudaStream_t s) {
-  auto k = k_scan_fast<C, W, U, VEC>;
+  auto k = k_scan_fast<C, W, U, VEC, 0>;
+  if constexpr (U == 0)
+    if (scan_mix(C) == 3) k = k_scan_fast<C, W, U, VEC, 3>;
   size_t smem = (size_t)C * W * 16 * 4;
   cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (attr_err != cudaSuccess) return attr_err;
+  // One wave of resident blocks (grid-stride): a grid above the occupancy
+  // limit leaves a tail wave running at a fraction of the SM (cls100: 80
+  // registers -> 3 blocks/SM, so the old 4/SM grid ran its last quarter alone).
+  int per_sm = 0;
+  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+  if (oe != cudaSuccess) return oe;
+  static const int bps = env_int("MDN_SCAN_BPS", 0);   // tuning knob: cap blocks/SM
+  if (bps > 0 && per_sm > bps) per_sm = bps;
+  if (per_sm < 1) per_sm = 1;
   int64_t blocks = (N + 255) / 256;
-  int64_t cap = (int64_t)dev_info().sms * (smem > 100000 ? 1 : smem > 60000 ? 2 : 4);
+  const int64_t cap = (int64_t)dev_info().sms * per_sm;
   if (blocks > cap) blocks = cap;
+  const bool pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
   k<<<(unsigned)blocks, 256, smem, s>>>(l.words, codes, N, l.M, sums, out, ldo, l.alpha_eff,
-                                        l.beta32, l.U == 0 ? 1 : l.U);
+                                        l.beta32, l.U == 0 ? 1 : l.U, pair);
   return cudaGetLastError();
 }
 

@@ -29,11 +29,29 @@ __device__ __forceinline__ uint32_t avg8(uint32_t a, uint32_t b) {
   return (a | b) - (x >> 1);
 }
 
-template <int C, int W, int U, bool UNROLL_G = false, class Words>
+// Pipe balancing. The exact accumulate is LOP/PRMT (split a word into its
+// even and odd byte lanes) + adds, all on the ALU pipe by default, which then
+// saturates (ncu: ALU 73%, issue 51% on cls100 mdn_scan) while the FMA pipe
+// idles. An add written as mad.lo with a multiplier ptxas cannot see (k_one,
+// a __constant__ 1 it cannot fold) stays an IMAD on the FMA pipe. Per pair of
+// words: ALU-only = 2 LDS + 6 ALU; IMAD form = 2 LDS + 4 ALU + 4 FMA. Mixing
+// one ALU-form word in three balances the two pipes against issue.
+static __constant__ uint32_t k_one = 1u;
+
+__device__ __forceinline__ uint32_t mad_add(uint32_t acc, uint32_t x, uint32_t one) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(one), "r"(acc));
+  return r;
+}
+
+// MIX (exact mode): 0 = ALU only; k > 0 = every k-th word on the ALU, the rest
+// IMAD adds.
+template <int C, int W, int U, bool UNROLL_G = false, int MIX = 0, class Words>
 __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Words words,
                                           uint32_t (&ae)[W], uint32_t (&ao)[W]) {
 #pragma unroll
   for (int w = 0; w < W; ++w) ae[w] = ao[w] = 0u;
+  const uint32_t one = k_one;
   if constexpr (U == 0) {
     constexpr int G = C >= 8 ? 8 : C;
     constexpr int NGU = UNROLL_G ? C / G : 1;
@@ -48,8 +66,13 @@ __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Word
 #pragma unroll
         for (int w = 0; w < W; ++w) {
           const uint32_t a = p0[w * 16], b = p1[w * 16];
-          ae[w] += (a & 0x00FF00FFu) + (b & 0x00FF00FFu);
-          ao[w] += __byte_perm(a, 0u, 0x4341) + __byte_perm(b, 0u, 0x4341);
+          if (MIX == 0 || w % (MIX > 0 ? MIX : 1) == 0) {
+            ae[w] += (a & 0x00FF00FFu) + (b & 0x00FF00FFu);
+            ao[w] += __byte_perm(a, 0u, 0x4341) + __byte_perm(b, 0u, 0x4341);
+          } else {
+            ae[w] = mad_add(mad_add(ae[w], a & 0x00FF00FFu, one), b & 0x00FF00FFu, one);
+            ao[w] = mad_add(mad_add(ao[w], __byte_perm(a, 0u, 0x4341), one), __byte_perm(b, 0u, 0x4341), one);
+          }
         }
       }
     }

@@ -242,3 +242,63 @@ print("chunked ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "chunked ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("mix", ["0", "3"])
+def test_scan_pipe_mix_subprocess(mix):
+    """mdn_scan's exact accumulate with every add on the ALU pipe (0) and with
+    two in three words' adds as IMADs on the FMA pipe (3), forced for every C:
+    sums and outputs bit-exact either way (the default picks per C)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle as O, paper_2106_10860_b200 as mdn
+from datagen.synth import make_config_data
+from helpers import model_bytes
+for name, C, M in (("cls100", 32, 100), ("cls10_c16", 16, 10), ("scale", 32, 16), ("tiny", 4, 4)):
+    blob = model_bytes(name); om = O.read_model(blob)
+    _, A, B = make_config_data(name, n_test=3001)
+    A = A[:3001]
+    model = mdn.mdn_model_load(blob, 0)
+    luts = mdn.mdn_build_luts(model, B, 0)
+    codes_o, S_o, want = O.amm(A, om, O.make_luts(om, B, "exact"))
+    codes = torch.from_numpy(O.pack_codes(codes_o)).cuda()
+    sums = torch.empty((3001, M), dtype=torch.int32, device="cuda")
+    out = torch.empty((3001, M), device="cuda")
+    mdn.mdn_scan(luts, codes, sums=sums, out=out)
+    assert (sums.cpu().numpy() == S_o).all(), name
+    assert (out.cpu().numpy().view(np.uint32) == want.view(np.uint32)).all(), name
+print("mix ok")
+'''
+    env = dict(os.environ, MDN_SCAN_MIX=mix)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env["PYTHONPATH"] = os.pathsep.join([root, os.path.join(root, "tests")])
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "mix ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name", ["cls10_c16", "scale", "tiny"])
+@pytest.mark.parametrize("layout", ["odd_ldo", "even_ldo", "misaligned"])
+def test_scan_strided_out(mdn, name, layout):
+    """mdn_scan's dequantised store with row stride ldo != M: 8-byte pair
+    stores only when M and ldo are even and out is 8-byte aligned, scalar
+    stores otherwise; nothing written outside the N x M window."""
+    model, om, A, B = _setup(mdn, name)
+    A = A[:2053]
+    n = A.shape[0]                     # tiny's test split has 2048 rows
+    spec = CONFIGS[name]
+    M = spec.M
+    luts = mdn.mdn_build_luts(model, B, 0)
+    codes_o, _, want = O.amm(A, om, O.make_luts(om, B, "exact"))
+    codes = torch.from_numpy(O.pack_codes(codes_o)).cuda()
+    ldo = {"odd_ldo": M + 1, "even_ldo": M + 2, "misaligned": M + 2}[layout]
+    off = 1 if layout == "misaligned" else 0
+    raw = torch.full((n * ldo + 2,), float("nan"), device="cuda")
+    out = raw[off:off + n * ldo].view(n, ldo)[:, :M]
+    mdn.mdn_scan(luts, codes, out=out)
+    _assert_out(out.cpu().numpy(), want)
+    rest = raw.clone()
+    rest[off:off + n * ldo].view(n, ldo)[:, :M] = 0
+    assert torch.isnan(rest[rest != 0]).all()
