@@ -543,7 +543,9 @@ def run(args):
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(f"{name}{'_col' if col else ''}_{args.mode}")
+                key = (f"{name}{'_col' if col else ''}{'' if op == 'amm' else '_' + op}"
+                       f"{'_pq' if pq else ''}_{args.mode}")
+                traffic = json.load(open(tp)).get(key)
             except Exception:
                 traffic = None
         line = {
