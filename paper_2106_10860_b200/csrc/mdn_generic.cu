@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "mdn_internal.h"
+#include "mdn_tma.cuh"
 
 namespace mdn {
 namespace {
@@ -144,7 +145,7 @@ __global__ void k_amm_generic(TreesDev t, LutsDev l, const TIn* __restrict__ A, 
 
 unsigned grid_for(int64_t N) {
   int64_t blocks = (N + GEN_THREADS - 1) / GEN_THREADS;
-  int64_t cap = 148 * 16;
+  const int64_t cap = (int64_t)fast::dev_info().sms * 16;   // grid-stride fallback kernels
   return (unsigned)(blocks < cap ? blocks : cap);
 }
 
