@@ -22,6 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                 "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+FLAGS += os.environ.get("MDN_NVCC_EXTRA", "").split()      # tuning experiments (-D...)
 
 
 def _sources():

@@ -11,5 +11,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 echo "launch list rc=$?"
 CMD2="python bench.py --steps 2 --warmup 1 --no-cpu-baseline"
 $CMD2 > gpurun_out/plain_full.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_amm -s 1 -c 1 -o gpurun_out/prof_cls100_exact $CMD2 > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_amm -s 1 -c 1 -f -o /tmp/prof_cls100_exact $CMD2 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
+python scripts/ncu_summary.py full /tmp/prof_cls100_exact.ncu-rep gpurun_out/ncu_full_cls100_exact_check.json > /dev/null 2>&1
