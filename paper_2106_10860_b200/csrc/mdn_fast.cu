@@ -60,10 +60,12 @@ __host__ __device__ constexpr int off_base(int c) { return 4 * c + 4 * (c >> 3);
 // 25 : 4W -- 2:8 for the 100-column tables, 6:4 for 10-16 columns, 8:2 for
 // <= 8 columns (ncu on the image config: scanners idle 63% at 2:8).
 // Exact-mode pipe mix of the scanner warps (mdn_scan.cuh) in the column-major
-// kernel, whose scanners bound cls100 (ALU pipe 75%). The row-major kernel
-// keeps ALU-only adds (the mix cost cls100 5% there).
+// kernel, whose scanners bound cls100 (ALU pipe 75%): on for the wide tables
+// only (same box, mix vs ALU-only: cls100 (W = 25) 4.14 -> 4.20e9 rows/s;
+// scale (W = 4) 1.04 -> 1.02e10, cls10_c16 -5%). The row-major kernel keeps
+// ALU-only adds (the mix cost cls100 5% there).
 #ifndef MDN_CM_MIX
-#define MDN_CM_MIX 0
+#define MDN_CM_MIX 3
 #endif
 
 template <int W, bool ENC_ONLY, bool CMV = false>
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
         const int64_t row = tile * BR + rl;
         const uint32_t* myc = s_codes + (b * BR + rl) * CBW;
         uint32_t ae[W], ao[W];
-        scan_core<C, W, U, false, SUBF == CM ? MDN_CM_MIX : 0>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
+        scan_core<C, W, U, false, (SUBF == CM && W >= 8) ? MDN_CM_MIX : 0>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
         if (k == KR - 1) mbar_arrive(&cempty[b]);
         if (row < p.N)
           store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32, p.pair);
