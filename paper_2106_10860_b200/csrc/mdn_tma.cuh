@@ -96,6 +96,7 @@ cudaError_t ensure_smem(const void* kernel, size_t smem);
 bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int SW, int R, int es);
 int knob_hint();
 bool knob_bq();
+int env_int(const char* name, int dflt);   // tuning knobs (mdn_fast.cu)
 
 }  // namespace fast
 }  // namespace mdn
