@@ -203,7 +203,18 @@ def test_bench_size_sampled_parity(mdn, name, n_rows):
         got = out.index_select(0, idx).cpu().numpy()
         _assert_out(got, O.amm(As, om, O.make_luts(om, B, mode, spec.U))[2])
         del out
-    del A
+    # the unfused halves at the same size, as bench.py --op encode / --op scan
+    codes = torch.empty((n_rows, (spec.C + 1) // 2), dtype=torch.uint8, device="cuda")
+    mdn.mdn_encode(model, A, codes)
+    luts = mdn.mdn_build_luts(model, B, 0)
+    out = torch.empty((n_rows, spec.M), device="cuda")
+    mdn.mdn_scan(luts, codes, out=out)
+    torch.cuda.synchronize()
+    idx = torch.from_numpy(rows).cuda()
+    codes_o, _, want = O.amm(A.index_select(0, idx).cpu().numpy(), om, O.make_luts(om, B, "exact"))
+    assert (codes.index_select(0, idx).cpu().numpy() == O.pack_codes(codes_o)).all()
+    _assert_out(out.index_select(0, idx).cpu().numpy(), want)
+    del A, codes, out
     torch.cuda.empty_cache()
 
 

@@ -139,7 +139,17 @@ def test_bench_size_sampled_parity(mdn, name):
         want = (O.amm_u8 if u8 else O.amm)(As, om, O.make_luts(om, B, mode, spec.U))[2]
         assert (_bits(got) == _bits(want)).all()
         del out
-    del A
+    # encode-only register-tree kernel + mdn_scan at the same size
+    codes = torch.empty((n, spec.C // 2), dtype=torch.uint8, device="cuda")
+    (mdn.mdn_encode_u8 if u8 else mdn.mdn_encode)(model, A, codes)
+    luts = mdn.mdn_build_luts(model, B, 0)
+    out = torch.empty((n, spec.M), device="cuda")
+    mdn.mdn_scan(luts, codes, out=out)
+    torch.cuda.synchronize()
+    codes_o, _, want = (O.amm_u8 if u8 else O.amm)(As, om, O.make_luts(om, B, "exact"))
+    assert (codes.index_select(0, idx).cpu().numpy() == O.pack_codes(codes_o)).all()
+    assert (_bits(out.index_select(0, idx).cpu().numpy()) == _bits(want)).all()
+    del A, codes, out
     torch.cuda.empty_cache()
 
 
