@@ -39,6 +39,21 @@ __device__ __forceinline__ float ld_stream(const float* p) {
   return v;
 }
 
+// RPT consecutive rows of one split column (At[col][row .. row + RPT)): one
+// vector load (RPT = 2: 8 B, 4: 16 B aligned), so a warp reads RPT x 128
+// contiguous bytes per column instead of 128.
+template <int RPT>
+__device__ __forceinline__ void ld_stream_v(const float* p, float (&v)[RPT]) {
+  if constexpr (RPT == 4) {
+    asm volatile("ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p));
+  } else if constexpr (RPT == 2) {
+    asm volatile("ld.global.cs.v2.f32 {%0, %1}, [%2];" : "=f"(v[0]), "=f"(v[1]) : "l"(p));
+  } else {
+    v[0] = ld_stream(p);
+  }
+}
+
 // Algorithm 1 (L228-248) for G codebooks of one row; x[i][t] = the row's value
 // in split column dims[c0 + i][t]. 0-based: p <- 2p + [x_t >= v^t_p].
 template <int G>
@@ -70,10 +85,63 @@ struct CmParams {
   float alpha_eff, beta32;
 };
 
-template <int C, int W, int U, bool VEC, bool ENC_ONLY>
-__global__ void __launch_bounds__(THREADS) k_amm_cm(const CmParams p) {
+// RPT consecutive rows row0 .. row0 + RPT - 1 (all < N) of one thread: each
+// split column is one vector load of the RPT values (RPT = 1: scalar).
+template <int C, int W, int U, bool VEC, bool ENC_ONLY, int RPT>
+__device__ __forceinline__ void cm_rows(const CmParams& p, int64_t row0, const float* s_thr,
+                                        const int64_t* s_col, const uint32_t* s_lut) {
   constexpr int G = C >= 8 ? 8 : C;
   constexpr int NG = C / G;
+  const float* a = p.At + row0;
+  uint32_t cw[RPT][NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    float x[RPT][G][4];
+#pragma unroll
+    for (int i = 0; i < G; ++i)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float v[RPT];
+        ld_stream_v<RPT>(a + s_col[(g * G + i) * 4 + t], v);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) x[r][i][t] = v[r];
+      }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) cw[r][g] = encode_group<G>(x[r], s_thr, g * G);
+  }
+  if constexpr (ENC_ONLY && RPT > 1 && C * RPT == 16) {
+    // the rows' codes are 8 contiguous bytes (C = 4: 4 rows x 2 B; C = 8:
+    // 2 rows x 4 B): one 8-byte store (the launcher checked the alignment)
+    uint64_t v = 0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) v |= (uint64_t)cw[r][0] << (r * 4 * C);
+    *reinterpret_cast<uint64_t*>(p.codes + row0 * (C / 2)) = v;
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int64_t row = row0 + r;
+    if constexpr (ENC_ONLY) {
+      if constexpr (C >= 8) {
+#pragma unroll
+        for (int g = 0; g < NG; ++g) reinterpret_cast<uint32_t*>(p.codes + row * (C / 2))[g] = cw[r][g];
+      } else if constexpr (C == 4) {
+        reinterpret_cast<uint16_t*>(p.codes + row * 2)[0] = (uint16_t)cw[r][0];
+      } else {
+        p.codes[row] = (uint8_t)cw[r][0];
+      }
+    } else {
+      uint32_t ae[W], ao[W];
+      scan_core<C, W, U, true>(s_lut, [&](int g) { return cw[r][g]; }, ae, ao);
+      store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32, p.pair);
+    }
+  }
+}
+
+// Thread per RPT consecutive rows (RPT > 1 for C <= 8 with 16-B / 8-B aligned
+// columns; the N % RPT tail rows then run one per thread).
+template <int C, int W, int U, bool VEC, bool ENC_ONLY, int RPT = 1>
+__global__ void __launch_bounds__(THREADS) k_amm_cm(const CmParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_thr = reinterpret_cast<float*>(smem);                       // [C][16]
   int64_t* s_col = reinterpret_cast<int64_t*>(s_thr + 16 * C);         // [C][4] element offsets
@@ -86,34 +154,14 @@ __global__ void __launch_bounds__(THREADS) k_amm_cm(const CmParams p) {
     for (int i = threadIdx.x; i < C * W * 4; i += blockDim.x) dst[i] = src[i];
   }
   __syncthreads();
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < p.N;
-       row += (int64_t)gridDim.x * blockDim.x) {
-    const float* a = p.At + row;
-    uint32_t cw[NG];
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      float x[G][4];
-#pragma unroll
-      for (int i = 0; i < G; ++i)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) x[i][t] = ld_stream(a + s_col[(g * G + i) * 4 + t]);
-      cw[g] = encode_group<G>(x, s_thr, g * G);
-    }
-    if constexpr (ENC_ONLY) {
-      if constexpr (C >= 8) {
-#pragma unroll
-        for (int g = 0; g < NG; ++g) reinterpret_cast<uint32_t*>(p.codes + row * (C / 2))[g] = cw[g];
-      } else if constexpr (C == 4) {
-        reinterpret_cast<uint16_t*>(p.codes + row * 2)[0] = (uint16_t)cw[0];
-      } else {
-        p.codes[row] = (uint8_t)cw[0];
-      }
-    } else {
-      uint32_t ae[W], ao[W];
-      scan_core<C, W, U, true>(s_lut, [&](int g) { return cw[g]; }, ae, ao);
-      store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32, p.pair);
-    }
-  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_full = p.N / RPT;
+  for (int64_t gi = tid; gi < n_full; gi += stride)
+    cm_rows<C, W, U, VEC, ENC_ONLY, RPT>(p, gi * RPT, s_thr, s_col, s_lut);
+  if constexpr (RPT > 1)
+    for (int64_t row = n_full * RPT + tid; row < p.N; row += stride)
+      cm_rows<C, W, U, VEC, ENC_ONLY, 1>(p, row, s_thr, s_col, s_lut);
 }
 
 // Generic fallback: any C (<= MAX_C), any M / U, any alignment.
@@ -168,9 +216,9 @@ __global__ void k_amm_cm_generic(TreesDev t, LutsDev l, const float* __restrict_
   }
 }
 
-template <int C, int W, int U, bool VEC, bool ENC>
+template <int C, int W, int U, bool VEC, bool ENC, int RPT = 1>
 cudaError_t launch(const CmParams& p, cudaStream_t s) {
-  auto k = k_amm_cm<C, W, U, VEC, ENC>;
+  auto k = k_amm_cm<C, W, U, VEC, ENC, RPT>;
   const size_t smem = 16 * C * 4 + 4 * C * 8 + (ENC ? 0 : (size_t)C * W * 16 * 4);
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
@@ -178,7 +226,7 @@ cudaError_t launch(const CmParams& p, cudaStream_t s) {
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  int64_t blocks = (p.N + THREADS - 1) / THREADS;
+  int64_t blocks = ((p.N + RPT - 1) / RPT + THREADS - 1) / THREADS;
   const int64_t cap = (int64_t)dev_info().sms * per_sm;
   if (blocks > cap) blocks = cap;
   k<<<(unsigned)blocks, THREADS, smem, s>>>(p);
@@ -219,6 +267,26 @@ static bool cm_ws_encode() {
   return v != 0;
 }
 
+// Rows per thread of k_amm_cm for C <= 8: 4 (C = 4) or 2 (C = 8) when the
+// columns allow the vector loads, else 1. MDN_CM_RPT=1 forces 1 (A/B only).
+static int cm_rpt(int C, const float* At, int64_t ldt) {
+  static int knob = [] { const char* e = getenv("MDN_CM_RPT"); return e ? atoi(e) : 0; }();
+  if (knob == 1 || C > 8) return 1;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(At);
+  if (C <= 4 && (a & 15u) == 0 && ldt % 4 == 0) return 4;
+  if ((a & 7u) == 0 && ldt % 2 == 0) return 2;
+  return 1;
+}
+
+template <int C, int W, int U, bool VEC, bool ENC>
+static cudaError_t launch_r(const CmParams& p, int rpt, cudaStream_t s) {
+  if constexpr (C <= 4)
+    if (rpt == 4) return launch<C, W, U, VEC, ENC, 4>(p, s);
+  if constexpr (C <= 8)
+    if (rpt >= 2) return launch<C, W, U, VEC, ENC, 2>(p, s);
+  return launch<C, W, U, VEC, ENC, 1>(p, s);
+}
+
 cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, int64_t N,
                           int64_t ldt, float* out, int64_t ldo, cudaStream_t s) {
   if (!cm_simple()) {
@@ -240,9 +308,10 @@ cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, 
   p.alpha_eff = l.alpha_eff;
   p.beta32 = l.beta32;
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  const int rpt = cm_rpt(t.C, At, ldt);
 #define X(c, w, u)                                                                   \
   if (t.C == c && l.W == w && l.U == u)                                              \
-    return vec ? launch<c, w, u, true, false>(p, s) : launch<c, w, u, false, false>(p, s);
+    return vec ? launch_r<c, w, u, true, false>(p, rpt, s) : launch_r<c, w, u, false, false>(p, rpt, s);
   MDN_CM_COMBOS(X)
 #undef X
   return cm_generic(t, &l, At, N, ldt, out, ldo, nullptr, s);
@@ -266,8 +335,9 @@ cudaError_t launch_encode_cm(const TreesDev& t, const float* At, int64_t N, int6
   const bool aligned = t.C >= 8 ? (ca & 3u) == 0 : (t.C == 4 ? (ca & 1u) == 0 : true);
   if (aligned) {
     switch (t.C) {
-      case 4: return launch<4, 1, 0, false, true>(p, s);
-      case 8: return launch<8, 1, 0, false, true>(p, s);
+      // several rows per thread only with 8-byte aligned codes (one store per group)
+      case 4: return launch_r<4, 1, 0, false, true>(p, (ca & 7u) ? 1 : cm_rpt(4, At, ldt), s);
+      case 8: return launch_r<8, 1, 0, false, true>(p, (ca & 7u) ? 1 : cm_rpt(8, At, ldt), s);
       case 16: return launch<16, 1, 0, false, true>(p, s);
       case 32: return launch<32, 1, 0, false, true>(p, s);
       case 64: return launch<64, 1, 0, false, true>(p, s);

@@ -138,3 +138,36 @@ def test_cm_slot_padding_and_repeated_dims(mdn):
     codes = torch.empty((A.shape[0], 8), dtype=torch.uint8, device="cuda")
     mdn.mdn_encode_cm(model, _At(A), codes)
     assert (codes.cpu().numpy() == O.pack_codes(codes_o)).all()
+
+
+@pytest.mark.parametrize("name", ["tiny", "image"])
+@pytest.mark.parametrize("N", [1, 3, 5, 1027, 70_001])
+@pytest.mark.parametrize("pad", [0, 1, 2])
+def test_cm_rows_per_thread(mdn, name, N, pad):
+    """k_amm_cm with several consecutive rows per thread (vector loads of a
+    split column): ragged N (N % 4 != 0 clamps the last group), and column
+    strides ldt = N + pad that allow 4-, 2- or only 1-row vectors."""
+    model, om, A, B = _setup(mdn, name)
+    A = np.concatenate([A] * (1 + N // A.shape[0]))[:N] if N > A.shape[0] else A[:N]
+    spec = CONFIGS[name]
+    luts = mdn.mdn_build_luts(model, B, 0)
+    codes_o, _, want = O.amm(A, om, O.make_luts(om, B, "exact"))
+    out = torch.full((N, spec.M), float("nan"), device="cuda")
+    mdn.mdn_amm_cm(model, luts, _At(A, pad=pad), out)
+    _assert_out(out.cpu().numpy(), want)
+    codes = torch.empty((N, spec.C // 2), dtype=torch.uint8, device="cuda")
+    mdn.mdn_encode_cm(model, _At(A, pad=pad), codes)
+    assert (codes.cpu().numpy() == O.pack_codes(codes_o)).all()
+
+
+@pytest.mark.parametrize("name", ["tiny", "image"])
+def test_cm_encode_unaligned_codes(mdn, name):
+    """mdn_encode_cm into codes that are not 8-byte aligned (the grouped 8-byte
+    code stores fall back to per-row stores)."""
+    model, om, A, B = _setup(mdn, name)
+    A = A[:4097]
+    N, nb = A.shape[0], CONFIGS[name].C // 2
+    raw = torch.zeros(N * nb + 8, dtype=torch.uint8, device="cuda")
+    codes = raw[nb:nb + N * nb].view(N, nb)          # offset by one row of codes
+    mdn.mdn_encode_cm(model, _At(A, pad=4), codes)
+    assert (codes.cpu().numpy() == O.pack_codes(O.encode(A, om))).all()
