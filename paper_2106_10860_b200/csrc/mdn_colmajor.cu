@@ -82,6 +82,7 @@ struct CmParams {
   uint8_t* codes;
   int M;
   bool pair;
+  bool pack2;             // M == 2, ldo == 2, out 16-B aligned: 2 rows per float4 store
   float alpha_eff, beta32;
 };
 
@@ -117,6 +118,21 @@ __device__ __forceinline__ void cm_rows(const CmParams& p, int64_t row0, const f
     for (int r = 0; r < RPT; ++r) v |= (uint64_t)cw[r][0] << (r * 4 * C);
     *reinterpret_cast<uint64_t*>(p.codes + row0 * (C / 2)) = v;
     return;
+  }
+  if constexpr (!ENC_ONLY && RPT == 2 && W == 1) {
+    if (p.pack2) {
+      // M = 2, ldo = 2: the two rows' outputs are 16 contiguous bytes
+      float4 o;
+      uint32_t ae[W], ao[W];
+      scan_core<C, W, U, true>(s_lut, [&](int g) { return cw[0][g]; }, ae, ao);
+      o.x = __fmaf_rn(p.alpha_eff, (float)(ae[0] & 0xFFFFu), p.beta32);
+      o.y = __fmaf_rn(p.alpha_eff, (float)(ao[0] & 0xFFFFu), p.beta32);
+      scan_core<C, W, U, true>(s_lut, [&](int g) { return cw[1][g]; }, ae, ao);
+      o.z = __fmaf_rn(p.alpha_eff, (float)(ae[0] & 0xFFFFu), p.beta32);
+      o.w = __fmaf_rn(p.alpha_eff, (float)(ao[0] & 0xFFFFu), p.beta32);
+      *reinterpret_cast<float4*>(p.out + row0 * 2) = o;
+      return;
+    }
   }
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
@@ -308,6 +324,7 @@ cudaError_t launch_amm_cm(const TreesDev& t, const LutsDev& l, const float* At, 
   p.alpha_eff = l.alpha_eff;
   p.beta32 = l.beta32;
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  p.pack2 = l.M == 2 && ldo == 2 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
   const int rpt = cm_rpt(t.C, At, ldt);
 #define X(c, w, u)                                                                   \
   if (t.C == c && l.W == w && l.U == u)                                              \

@@ -10,7 +10,7 @@ run default
 for cfg in cls100 cls10_c16 cls10_c32 cls10_c64 scale tiny image image_u8; do
   for mode in exact avg; do run ${cfg}_${mode} --config $cfg --mode $mode --no-cpu-baseline; done
 done
-for cfg in cls100 scale cls10_c16 tiny; do
+for cfg in cls100 scale cls10_c16 tiny image; do
   for mode in exact avg; do run col_${cfg}_${mode} --config $cfg --mode $mode --layout col --no-cpu-baseline; done
 done
 for cfg in cls100 cls10_c16 cls10_c32 cls10_c64 scale tiny image; do
@@ -19,7 +19,7 @@ for cfg in cls100 cls10_c16 cls10_c32 cls10_c64 scale tiny image; do
 done
 run encode_image_u8 --config image_u8 --op encode --no-cpu-baseline
 run scan_cls100_avg --config cls100 --op scan --mode avg --no-cpu-baseline
-for cfg in cls100 scale cls10_c16; do run encode_col_${cfg} --config $cfg --op encode --layout col --no-cpu-baseline; done
+for cfg in cls100 scale cls10_c16 tiny image; do run encode_col_${cfg} --config $cfg --op encode --layout col --no-cpu-baseline; done
 for cfg in cls100 cls10_c16 scale tiny; do run pq_encode_${cfg} --config $cfg --op encode --encoder pq --no-cpu-baseline; done
 run pq_amm_cls100 --config cls100 --encoder pq --no-cpu-baseline
 for cfg in tiny cls10_c16 cls100 scale image; do run train_${cfg} --config $cfg --op train --steps 3 --warmup 1 --cpu-seconds 5; done

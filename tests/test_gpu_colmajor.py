@@ -155,6 +155,10 @@ def test_cm_rows_per_thread(mdn, name, N, pad):
     out = torch.full((N, spec.M), float("nan"), device="cuda")
     mdn.mdn_amm_cm(model, luts, _At(A, pad=pad), out)
     _assert_out(out.cpu().numpy(), want)
+    wide = torch.full((N, spec.M + 2), float("nan"), device="cuda")   # ldo != M: per-row stores
+    mdn.mdn_amm_cm(model, luts, _At(A, pad=pad), wide[:, :spec.M])
+    _assert_out(wide[:, :spec.M].cpu().numpy(), want)
+    assert torch.isnan(wide[:, spec.M:]).all()
     codes = torch.empty((N, spec.C // 2), dtype=torch.uint8, device="cuda")
     mdn.mdn_encode_cm(model, _At(A, pad=pad), codes)
     assert (codes.cpu().numpy() == O.pack_codes(codes_o)).all()
