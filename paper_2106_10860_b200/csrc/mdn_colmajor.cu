@@ -33,11 +33,8 @@ namespace colmajor {
 
 constexpr int THREADS = 256;
 
-__device__ __forceinline__ float ld_stream(const float* p) {
-  float v;
-  asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  return v;
-}
+// Streaming (evict-first) loads.
+__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
 
 // RPT consecutive rows of one split column (At[col][row .. row + RPT)): one
 // vector load (RPT = 2: 8 B, 4: 16 B aligned), so a warp reads RPT x 128
@@ -45,10 +42,11 @@ __device__ __forceinline__ float ld_stream(const float* p) {
 template <int RPT>
 __device__ __forceinline__ void ld_stream_v(const float* p, float (&v)[RPT]) {
   if constexpr (RPT == 4) {
-    asm volatile("ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p));
+    const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+    v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
   } else if constexpr (RPT == 2) {
-    asm volatile("ld.global.cs.v2.f32 {%0, %1}, [%2];" : "=f"(v[0]), "=f"(v[1]) : "l"(p));
+    const float2 t = __ldcs(reinterpret_cast<const float2*>(p));
+    v[0] = t.x, v[1] = t.y;
   } else {
     v[0] = ld_stream(p);
   }
@@ -86,39 +84,12 @@ struct CmParams {
   float alpha_eff, beta32;
 };
 
-// RPT consecutive rows row0 .. row0 + RPT - 1 (all < N) of one thread: each
-// split column is one vector load of the RPT values (RPT = 1: scalar).
+// Per-row code stores (encode) or scan + dequantised stores (fused).
 template <int C, int W, int U, bool VEC, bool ENC_ONLY, int RPT>
-__device__ __forceinline__ void cm_rows(const CmParams& p, int64_t row0, const float* s_thr,
-                                        const int64_t* s_col, const uint32_t* s_lut) {
-  constexpr int G = C >= 8 ? 8 : C;
-  constexpr int NG = C / G;
-  const float* a = p.At + row0;
-  uint32_t cw[RPT][NG];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    float x[RPT][G][4];
-#pragma unroll
-    for (int i = 0; i < G; ++i)
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        float v[RPT];
-        ld_stream_v<RPT>(a + s_col[(g * G + i) * 4 + t], v);
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) x[r][i][t] = v[r];
-      }
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) cw[r][g] = encode_group<G>(x[r], s_thr, g * G);
-  }
-  if constexpr (ENC_ONLY && RPT > 1 && C * RPT == 16) {
-    // the rows' codes are 8 contiguous bytes (C = 4: 4 rows x 2 B; C = 8:
-    // 2 rows x 4 B): one 8-byte store (the launcher checked the alignment)
-    uint64_t v = 0;
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) v |= (uint64_t)cw[r][0] << (r * 4 * C);
-    *reinterpret_cast<uint64_t*>(p.codes + row0 * (C / 2)) = v;
-    return;
-  }
+__device__ __forceinline__ void cm_store(const CmParams& p, int64_t row0,
+                                         const uint32_t (&cw)[RPT][C >= 8 ? C / 8 : 1],
+                                         const uint32_t* s_lut) {
+  constexpr int NG = C >= 8 ? C / 8 : 1;
   if constexpr (!ENC_ONLY && RPT == 2 && W == 1) {
     if (p.pack2) {
       // M = 2, ldo = 2: the two rows' outputs are 16 contiguous bytes
@@ -154,10 +125,50 @@ __device__ __forceinline__ void cm_rows(const CmParams& p, int64_t row0, const f
   }
 }
 
+// RPT consecutive rows row0 .. row0 + RPT - 1 (all < N) of one thread: each
+// split column is one vector load of the RPT values (RPT = 1: scalar).
+template <int C, int W, int U, bool VEC, bool ENC_ONLY, int RPT>
+__device__ __forceinline__ void cm_rows(const CmParams& p, int64_t row0, const float* s_thr,
+                                        const int64_t* s_col, const uint32_t* s_lut) {
+  constexpr int G = C >= 8 ? 8 : C;
+  constexpr int NG = C / G;
+  const float* a = p.At + row0;
+  uint32_t cw[RPT][NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    float x[RPT][G][4];
+#pragma unroll
+    for (int i = 0; i < G; ++i)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float v[RPT];
+        ld_stream_v<RPT>(a + s_col[(g * G + i) * 4 + t], v);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) x[r][i][t] = v[r];
+      }
+    // every split-column load of the group is issued before the first tree
+    // consumes one (left alone, the compiler interleaved them at 38 registers
+    // in the fused variant: long-scoreboard stalls 18 per issue)
+    asm volatile("" ::: "memory");
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) cw[r][g] = encode_group<G>(x[r], s_thr, g * G);
+  }
+  if constexpr (ENC_ONLY && RPT > 1 && C * RPT == 16) {
+    // the rows' codes are 8 contiguous bytes (C = 4: 4 rows x 2 B; C = 8:
+    // 2 rows x 4 B): one 8-byte store (the launcher checked the alignment)
+    uint64_t v = 0;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) v |= (uint64_t)cw[r][0] << (r * 4 * C);
+    *reinterpret_cast<uint64_t*>(p.codes + row0 * (C / 2)) = v;
+  } else {
+    cm_store<C, W, U, VEC, ENC_ONLY, RPT>(p, row0, cw, s_lut);
+  }
+}
+
 // Thread per RPT consecutive rows (RPT > 1 for C <= 8 with 16-B / 8-B aligned
 // columns; the N % RPT tail rows then run one per thread).
 template <int C, int W, int U, bool VEC, bool ENC_ONLY, int RPT = 1>
-__global__ void __launch_bounds__(THREADS) k_amm_cm(const CmParams p) {
+__global__ void __launch_bounds__(THREADS, 1) k_amm_cm(const CmParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_thr = reinterpret_cast<float*>(smem);                       // [C][16]
   int64_t* s_col = reinterpret_cast<int64_t*>(s_thr + 16 * C);         // [C][4] element offsets
