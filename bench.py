@@ -259,6 +259,26 @@ def run_train(args):
         blob = mdn.mdn_train(A, spec.C, 1.0)                 # synchronous
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
+    # Kernel launches of one training call, counted by the CUDA profiler on an
+    # extra untimed call: the library's own kernels (namespace mdn) and the
+    # library-routine kernels it calls (CUB segmented sort, cuSOLVER).
+    launches = None
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            mdn.mdn_train(A, spec.C, 1.0)
+            torch.cuda.synchronize()
+        ours = lib = 0
+        for ev in prof.events():
+            if ev.device_type.name != "CUDA" or "memcpy" in ev.name.lower() or "memset" in ev.name.lower():
+                continue
+            if "mdn::" in ev.name or "fast::" in ev.name:
+                ours += 1
+            else:
+                lib += 1
+        launches = {"ours_per_call": ours, "library_per_call": lib}
+    except Exception as e:  # pragma: no cover - profiler unavailable
+        launches = {"error": str(e)[:200]}
     cpu = None
     if not args.no_cpu_baseline:
         import oracle as O
@@ -281,7 +301,10 @@ def run_train(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{name} training split, trees + ridge prototypes (lambda = 1)",
                        "rows": int(A_h.shape[0])},
-            "roofline": None, "cpu_baseline": cpu, "e2e": None, "gpu_launches": None,
+            "roofline": None, "cpu_baseline": cpu, "e2e": None,
+            "gpu_launches": (launches["ours_per_call"] * args.steps
+                             if launches and "ours_per_call" in launches else None),
+            "launches_per_call": launches,
             "op": "train", "model_bytes": len(blob),
             "note": "offline step, untimed in the paper (L379); wall time of the synchronous call"}
     print(json.dumps(line), flush=True)
@@ -546,6 +569,22 @@ def run(args):
         except Exception as e:  # pragma: no cover - host without fork
             cpu["all_cores"] = {"error": str(e)[:200]}
 
+    # gpu_launches evidence: the CUDA profiler's kernel list of one extra,
+    # untimed step (the library's kernels live in namespace mdn).
+    prof_kernels = None
+    if rank == 0:
+        try:
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                step()
+                torch.cuda.synchronize()
+            names = [e.name for e in prof.events() if e.device_type.name == "CUDA"
+                     and "memcpy" not in e.name.lower() and "memset" not in e.name.lower()]
+            prof_kernels = {"ours_per_step": sum(("mdn::" in n or "fast::" in n) for n in names),
+                            "other_per_step": sum(not ("mdn::" in n or "fast::" in n) for n in names),
+                            "names": sorted({n.split("(")[0][:80] for n in names})}
+        except Exception as e:  # pragma: no cover - profiler unavailable
+            prof_kernels = {"error": str(e)[:200]}
     if rank == 0:
         traffic = None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -589,6 +628,7 @@ def run(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * (2 if pq and op == "amm" else 1),
+            "gpu_launches_profiled": prof_kernels,
             "op": op,
             "clocks": clocks,
             "nmse_vs_exact_fp64": nmse,
