@@ -50,6 +50,9 @@ constexpr int NG = 2;                    // worker groups
 constexpr int NWK = NG * CPS;            // worker warps
 constexpr int THREADS = 32 * (1 + NWK);
 constexpr int NS_MAX = 8;
+#ifndef MDN_RT_CTAS_U8
+#define MDN_RT_CTAS_U8 1     // resident CTAs per SM of the 8-bit variants (tuning: -DMDN_RT_CTAS_U8=2)
+#endif
 
 struct SParams {
   int64_t N, n_tiles, ldo;
@@ -174,7 +177,7 @@ __device__ __forceinline__ float u16_to_f(uint32_t s) {
 // their nibbles together with shuffles and one lane stores the row's packed
 // codes; no tables, no scan.
 template <class TIn, int D, int C, int W2, int U, int VEC, bool BQ, bool ENC = false>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1)
     k_amm_rt(const __grid_constant__ CUtensorMap tmap, const SParams p) {
   // Shared row pitch (elements): fp32 rows D + 4 (pitch == 4 mod 32 words);
   // 8-bit rows D bytes unpadded, so the encoder's 4-row x 8-codebook word
@@ -433,7 +436,8 @@ cudaError_t launch(const CUtensorMap& tm, const SParams& p, size_t smem, cudaStr
   auto k = k_amm_rt<TIn, 32, C, W2, U, VEC, BQ>;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
-  const int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
+  const int64_t cap = (int64_t)dev_info().sms * (sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1);
+  const int64_t grid = p.n_tiles < cap ? p.n_tiles : cap;
   k<<<(unsigned)grid, THREADS, smem, st>>>(tm, p);
   return cudaGetLastError();
 }
@@ -443,7 +447,8 @@ cudaError_t launch_enc(const CUtensorMap& tm, const SParams& p, size_t smem, cud
   auto k = k_amm_rt<TIn, 32, C, 1, 0, 0, BQ, true>;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
-  const int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
+  const int64_t cap = (int64_t)dev_info().sms * (sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1);
+  const int64_t grid = p.n_tiles < cap ? p.n_tiles : cap;
   k<<<(unsigned)grid, THREADS, smem, st>>>(tm, p);
   return cudaGetLastError();
 }
@@ -488,7 +493,8 @@ static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int
   const int stage_b = ((R * pitch_e * es) + 127) & ~127;
   const int W2 = (l.M + 1) / 2;
   const size_t fixed = ((256 + (size_t)t.C * 16 * W2 * 4 + (size_t)NWK * 32 * (t.C == 8 ? 12 : 4) * 4) + 127) & ~size_t(127);
-  const size_t budget = (size_t)dev_info().smem_optin;
+  size_t budget = (size_t)dev_info().smem_optin;
+  if (es == 1 && MDN_RT_CTAS_U8 > 1) budget = std::min(budget, (size_t)(233472 / MDN_RT_CTAS_U8 - 1024));
   if (fixed + (size_t)2 * NG * stage_b > budget) return cudaSuccess;
   int NS = (int)((budget - fixed) / stage_b);
   if (NS > NS_MAX) NS = NS_MAX;
@@ -544,7 +550,8 @@ static cudaError_t encode_rt(const TreesDev& t, const TIn* A, int64_t N, int64_t
   const int pitch_e = es == 1 ? t.D : t.D + 16 / es;
   const int stage_b = ((R * pitch_e * es) + 127) & ~127;
   const size_t fixed = 256;                          // barriers only (kernel's OFF_STAGE)
-  const size_t budget = (size_t)dev_info().smem_optin;
+  size_t budget = (size_t)dev_info().smem_optin;
+  if (es == 1 && MDN_RT_CTAS_U8 > 1) budget = std::min(budget, (size_t)(233472 / MDN_RT_CTAS_U8 - 1024));
   int NS = (int)((budget - fixed) / stage_b);
   if (NS > NS_MAX) NS = NS_MAX;
   NS -= NS % NG;
