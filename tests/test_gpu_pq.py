@@ -95,3 +95,25 @@ def test_pq_model_state_errors(mdn):
     out = torch.empty((64, 4), device="cuda")
     with pytest.raises(mdn.MdnError):
         mdn.mdn_amm(model, luts, dA, out)
+
+
+@pytest.mark.parametrize("base", ["cls100", "tiny"])
+def test_encode_pq_bench_size_sampled(mdn, base):
+    """The PQ encoder at the bench size, on the rows bench.py --encoder pq
+    generates (cls100: 2^21, tiny: 2^25); 65536 sampled rows + the tail vs the
+    oracle, bit-exact codes."""
+    import bench
+    model, om, _, _ = _setup(mdn, base)
+    A = bench._bench_rows(base, 0, 1, "cuda")
+    n = A.shape[0]
+    codes = torch.empty((n, om.C // 2), dtype=torch.uint8, device="cuda")
+    mdn.mdn_encode_pq(model, A, codes)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(99)
+    rows = np.unique(np.concatenate([rng.integers(0, n, 65536), np.arange(n - 300, n)]))
+    idx = torch.from_numpy(rows).cuda()
+    got = codes.index_select(0, idx).cpu().numpy()
+    want = O.pack_codes(O.encode_pq(A.index_select(0, idx).cpu().numpy(), om))
+    assert (got == want).all(), f"{(got != want).sum()} code bytes differ"
+    del A, codes
+    torch.cuda.empty_cache()
