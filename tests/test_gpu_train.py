@@ -92,3 +92,23 @@ def test_train_errors(mdn):
     n = ct.c_size_t(0)
     assert m._lib.mdn_train(None, 0, 0, 32, 4, 1.0, 0, None, ct.byref(n)) == 0
     assert n.value == 48 + 76 * 4 + 64 * 4 * 32 + 8
+
+
+@pytest.mark.parametrize("name,codebooks", [("cls100", [0, 17]), ("image", [0])])
+def test_train_bench_size_sampled_codebooks(mdn, name, codebooks):
+    """mdn_train on the full training split bench.py --op train uses (cls100:
+    50,000 x 512, C = 32; image: 1,000,000 8-bit patches as fp32, C = 8);
+    sampled codebooks re-learned by the oracle (Alg. 2-4) on the same rows:
+    identical split dims and thresholds (image: integer data, exact sums;
+    cls100: fp32, identical on these inputs, else the per-level losses would
+    have to agree to 1e-9)."""
+    from datagen.synth import CONFIGS
+    spec = CONFIGS[name]
+    A = make_config_data(name, n_test=0)[0].astype(np.float32)
+    got = _gpu_train(mdn, A, spec.C, 1.0)
+    assert got.n_train == A.shape[0]
+    for c in codebooks:
+        b, e = got.sub[c]
+        dims, thr, _, losses = O.learn_hash_tree(A[:, b:e])
+        assert (got.dims[c] == dims + b).all(), (c, got.dims[c], dims + b)
+        assert (got.thr[c].view(np.uint32) == thr.view(np.uint32)).all(), c
