@@ -1,5 +1,6 @@
 """GPU parity over shapes the BASELINE configs do not reach: odd C, D not a
-multiple of 4 (generic encode), M from 1 to 300 (W up to 75: generic scan),
+multiple of 4 (generic encode), C up to MAX_C = 256, M from 1 to 1000 (W up
+to 250: generic scan, tables beyond shared memory),
 every averaging block U, non-contiguous outputs. Models are trained on the fly
 by the oracle on small relu low-rank data."""
 import numpy as np
@@ -42,6 +43,8 @@ def _check(got, want):
 SHAPES = [  # (C, D, M)
     (1, 8, 3), (2, 8, 1), (3, 10, 7), (6, 30, 5), (12, 48, 33), (4, 32, 300),
     (16, 64, 10), (8, 32, 2), (32, 128, 16), (128, 256, 4), (64, 512, 12),
+    (256, 256, 5),      # MAX_C codebooks of one dim each (S <= 255 C < 2^16)
+    (8, 32, 1000),      # M = 1000: 250 table words per code, tables beyond shared memory
 ]
 
 
