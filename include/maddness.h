@@ -218,6 +218,14 @@ int mdn_amm_host(mdn_exec* exec, const float* A_host, int64_t N, int64_t lda,
  * u8 N x D (lda bytes) -- a quarter of the host->device bytes per row. */
 int mdn_amm_host_u8(mdn_exec* exec, const uint8_t* A_host, int64_t N, int64_t lda,
                     float* out_host, int64_t ldo);
+/* The same pipeline for column-major host A (mdn_amm_cm; SURVEY N2, P:L246,
+ * P:L431): At_host fp32 D x N, row stride ldt >= N (column n of A = row n of
+ * the result). Per chunk only the model's distinct split columns of At are
+ * copied host->device (4 |S| bytes per row instead of 4 D), into the slot
+ * buffer used as a D x chunk_rows column-major tile. Same errors as
+ * mdn_amm_host; ldt < N -> MDN_EINVAL. */
+int mdn_amm_cm_host(mdn_exec* exec, const float* At_host, int64_t N, int64_t ldt,
+                    float* out_host, int64_t ldo);
 
 /* --------------------------------------------------------- diagnostics -- */
 

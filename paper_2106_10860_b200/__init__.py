@@ -59,6 +59,7 @@ _SIGS = {
     "mdn_amm_cm": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "mdn_encode_pq": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "mdn_amm_host_u8": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64]),
+    "mdn_amm_cm_host": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64]),
     "mdn_train": (_i32, [_vp, _i64, _i64, _i32, _i32, ct.c_double, _i32, _vp, ct.POINTER(_sz)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -356,6 +357,20 @@ def mdn_amm_host_u8(ex: Exec, A_host, out_host):
     if so[0] != sa[0]:
         raise ValueError("row count mismatch")
     _check(_lib.mdn_amm_host_u8(ex._h, pa, sa[0], lda, po, ldo), "mdn_amm_host_u8")
+    return out_host
+
+
+def mdn_amm_cm_host(ex: Exec, At_host, out_host):
+    """Host-buffer pipeline for column-major A: At_host float32
+    D x N (numpy or CPU tensor, unit column stride, row stride >= N); only the
+    model's split columns are copied to the device."""
+    pa, ldt, sa = _host_ptr(At_host, "At_host")
+    po, ldo, so = _host_ptr(out_host, "out_host")
+    if sa[0] != ex._model.D:
+        raise ValueError("At_host must be D x N")
+    if so[0] != sa[1]:
+        raise ValueError("row count mismatch")
+    _check(_lib.mdn_amm_cm_host(ex._h, pa, sa[1], ldt, po, ldo), "mdn_amm_cm_host")
     return out_host
 
 

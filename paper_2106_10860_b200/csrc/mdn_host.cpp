@@ -784,4 +784,49 @@ int mdn_amm_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, float
   return amm_host<uint8_t>(x, A, N, lda, out, ldo);
 }
 
+// Column-major host A: per chunk only the distinct split columns
+// cross PCIe (4 |S| instead of 4 D bytes per row). The slot buffer is used as
+// a D x chunk column-major tile (ldt = chunk); rows of At that are not split
+// columns are never copied and never read. Consecutive split columns go as
+// one 2-D copy (rows of n floats, pitches ldt and chunk).
+int mdn_amm_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, float* out,
+                    int64_t ldo) {
+  if (!x || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  const int M = x->luts->M;
+  if (!At || !out || ldt < N || ldo < M) return MDN_EINVAL;
+  DeviceGuard g(x->device);
+  if (!g.ok) return MDN_ECUDA;
+  const std::vector<uint16_t>& cols = x->model->h_cols;
+  cudaError_t e = cudaSuccess;
+  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
+  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
+    const int s = (int)(q % x->n_slots);
+    cudaStream_t st = x->streams[s];
+    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
+    float* dAt = x->dA[s];
+    for (size_t i = 0; i < cols.size() && e == cudaSuccess;) {
+      size_t j = i + 1;
+      while (j < cols.size() && cols[j] == cols[j - 1] + 1) ++j;     // run of adjacent columns
+      const int64_t c0 = cols[i];
+      e = cudaMemcpy2DAsync(dAt + c0 * x->chunk, (size_t)x->chunk * sizeof(float),
+                            At + c0 * ldt + r0, (size_t)ldt * sizeof(float),
+                            (size_t)n * sizeof(float), j - i, cudaMemcpyHostToDevice, st);
+      i = j;
+    }
+    if (e != cudaSuccess) break;
+    e = launch_amm_cm(x->model->trees(), x->luts->dev(), dAt, n, x->chunk, x->dOut[s], M, st);
+    if (e != cudaSuccess) break;
+    e = ldo == M ? cudaMemcpyAsync(out + r0 * ldo, x->dOut[s], (size_t)n * M * sizeof(float),
+                                   cudaMemcpyDeviceToHost, st)
+                 : cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
+                                     M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
+  }
+  for (auto s : x->streams) {
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+  }
+  return cuda_status(e);
+}
+
 }  // extern "C"

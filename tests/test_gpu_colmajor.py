@@ -175,3 +175,24 @@ def test_cm_encode_unaligned_codes(mdn, name):
     codes = raw[nb:nb + N * nb].view(N, nb)          # offset by one row of codes
     mdn.mdn_encode_cm(model, _At(A, pad=4), codes)
     assert (codes.cpu().numpy() == O.pack_codes(O.encode(A, om))).all()
+
+
+@pytest.mark.parametrize("name,chunk", [("cls100", 1536), ("cls10_c16", 1001), ("tiny", 4096)])
+def test_cm_host_executor(mdn, name, chunk):
+    """mdn_amm_cm_host: column-major host A through the pipelined executor
+    (only split columns cross PCIe), ragged last chunk, ldt > N, ldo > M,
+    chunk sizes with and without 16-byte column alignment on the device."""
+    model, om, A, B = _setup(mdn, name)
+    A = A[:5003]
+    N = A.shape[0]
+    spec = CONFIGS[name]
+    luts = mdn.mdn_build_luts(model, B, 1, spec.U)
+    want = O.amm(A, om, O.make_luts(om, B, "avg", spec.U))[2]
+    At_h = torch.zeros((spec.D, N + 7)).pin_memory()
+    At_h[:, :N] = torch.from_numpy(np.ascontiguousarray(A.T))
+    out_h = torch.full((N, spec.M + 3), float("nan")).pin_memory()
+    ex = mdn.mdn_exec_create(model, luts, chunk_rows=chunk, n_slots=3)
+    mdn.mdn_amm_cm_host(ex, At_h[:, :N], out_h[:, :spec.M])
+    ex.close()
+    _assert_out(out_h[:, :spec.M].numpy(), want)
+    assert torch.isnan(out_h[:, spec.M:]).all()
