@@ -549,6 +549,36 @@ def run(args):
                + " (pinned host A -> 3-slot pipelined H2D/kernel/D2H)"}
         ex.close()
         del A_h, out_h
+    elif op in ("encode", "scan") and not col and not pq and not u8 and (rank == 0 or ws > 1):
+        # the unfused halves through host buffers (mdn_encode_host / mdn_scan_host)
+        nb = (spec.C + 1) // 2
+        ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
+                                 n_slots=3)
+        n_e2e = min(n, (1 << 30) // (4 * spec.D))
+        if op == "encode":
+            A_h = A[:n_e2e].cpu().pin_memory()
+            c_h = torch.empty((n_e2e, nb), dtype=torch.uint8).pin_memory()
+            host_call = lambda: mdn.mdn_encode_host(ex, A_h, c_h)
+            h2d, d2h = n_e2e * 4 * spec.D, n_e2e * nb
+        else:
+            c_h = codes[:n_e2e].cpu().pin_memory()
+            A_h = torch.empty((n_e2e, spec.M), dtype=torch.float32).pin_memory()   # out
+            host_call = lambda: mdn.mdn_scan_host(ex, c_h, A_h)
+            h2d, d2h = n_e2e * nb, n_e2e * 4 * spec.M
+        host_call()                                           # warm-up
+        e2e_steps = max(1, min(args.steps, 3))
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            host_call()
+        t_e2e = allreduce_max(time.perf_counter() - t0)
+        e2e = {"value": n_e2e * ws * e2e_steps / t_e2e, "unit": "rows/s",
+               "rows_per_step": n_e2e * ws, "h2d_bytes_per_step": h2d * ws,
+               "d2h_bytes_per_step": d2h * ws, "steps": e2e_steps,
+               "path": f"mdn_{op}_host (pinned host buffers -> 3-slot pipelined H2D/kernel/D2H)"}
+        ex.close()
+        del A_h, c_h
     elif op == "amm" and col and not pq and (rank == 0 or ws > 1):
         # column-major host A: only the split columns cross PCIe (N2)
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=1 << 18, n_slots=3)

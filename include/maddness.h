@@ -218,6 +218,14 @@ int mdn_amm_host(mdn_exec* exec, const float* A_host, int64_t N, int64_t lda,
  * u8 N x D (lda bytes) -- a quarter of the host->device bytes per row. */
 int mdn_amm_host_u8(mdn_exec* exec, const uint8_t* A_host, int64_t N, int64_t lda,
                     float* out_host, int64_t ldo);
+/* The unfused halves through the same executor (slots, streams): g on host
+ * rows -> host codes (codes_host u8 N x ceil(C/2), contiguous), and f on host
+ * codes -> host out (fp32 N x M, ldo >= M) with the executor's tables. Same
+ * errors as mdn_amm_host. */
+int mdn_encode_host(mdn_exec* exec, const float* A_host, int64_t N, int64_t lda,
+                    uint8_t* codes_host);
+int mdn_scan_host(mdn_exec* exec, const uint8_t* codes_host, int64_t N, float* out_host,
+                  int64_t ldo);
 /* The same pipeline for column-major host A (mdn_amm_cm; SURVEY N2, P:L246,
  * P:L431): At_host fp32 D x N, row stride ldt >= N (column n of A = row n of
  * the result). Per chunk only the model's distinct split columns of At are

@@ -60,6 +60,8 @@ _SIGS = {
     "mdn_encode_pq": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "mdn_amm_host_u8": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64]),
     "mdn_amm_cm_host": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64]),
+    "mdn_encode_host": (_i32, [_vp, _vp, _i64, _i64, _vp]),
+    "mdn_scan_host": (_i32, [_vp, _vp, _i64, _vp, _i64]),
     "mdn_train": (_i32, [_vp, _i64, _i64, _i32, _i32, ct.c_double, _i32, _vp, ct.POINTER(_sz)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -357,6 +359,36 @@ def mdn_amm_host_u8(ex: Exec, A_host, out_host):
     if so[0] != sa[0]:
         raise ValueError("row count mismatch")
     _check(_lib.mdn_amm_host_u8(ex._h, pa, sa[0], lda, po, ldo), "mdn_amm_host_u8")
+    return out_host
+
+
+def _host_u8(x, what):
+    import torch
+    if isinstance(x, np.ndarray) and x.dtype == np.uint8 and x.ndim == 2 and x.flags["C_CONTIGUOUS"]:
+        return x.ctypes.data, x.shape
+    if isinstance(x, torch.Tensor) and not x.is_cuda and x.dtype == torch.uint8 and x.dim() == 2 \
+            and x.is_contiguous():
+        return x.data_ptr(), tuple(x.shape)
+    raise TypeError(f"{what} must be a contiguous 2-D host uint8 array")
+
+
+def mdn_encode_host(ex: Exec, A_host, codes_host):
+    """g through the executor: host fp32 rows -> host packed codes."""
+    pa, lda, sa = _host_ptr(A_host, "A_host")
+    pc, sc = _host_u8(codes_host, "codes_host")
+    if sc != (sa[0], (ex._model.C + 1) // 2):
+        raise ValueError("codes_host must be N x ceil(C/2)")
+    _check(_lib.mdn_encode_host(ex._h, pa, sa[0], lda, pc), "mdn_encode_host")
+    return codes_host
+
+
+def mdn_scan_host(ex: Exec, codes_host, out_host):
+    """f through the executor: host packed codes -> host fp32 out."""
+    pc, sc = _host_u8(codes_host, "codes_host")
+    po, ldo, so = _host_ptr(out_host, "out_host")
+    if sc[1] != (ex._model.C + 1) // 2 or so[0] != sc[0]:
+        raise ValueError("codes_host N x ceil(C/2), out_host N x M")
+    _check(_lib.mdn_scan_host(ex._h, pc, sc[0], po, ldo), "mdn_scan_host")
     return out_host
 
 

@@ -679,6 +679,7 @@ struct mdn_exec {
   int n_slots;
   std::vector<cudaStream_t> streams;
   std::vector<float*> dA, dOut;
+  std::vector<uint8_t*> dC;       // packed codes of a chunk (mdn_encode_host / mdn_scan_host)
 };
 
 void mdn_exec_free(mdn_exec* x) {
@@ -688,6 +689,7 @@ void mdn_exec_free(mdn_exec* x) {
     for (auto s : x->streams) cudaStreamDestroy(s);
     for (auto p : x->dA) cudaFree(p);
     for (auto p : x->dOut) cudaFree(p);
+    for (auto p : x->dC) cudaFree(p);
   }
   delete x;
 }
@@ -715,10 +717,13 @@ int mdn_exec_create(const mdn_model* m, const mdn_luts* l, int64_t chunk_rows, i
       return MDN_ECUDA;
     }
     x->streams.push_back(s);
+    uint8_t* c = nullptr;
     int st = dalloc(&a, (size_t)chunk_rows * m->D);
     if (st == MDN_OK) st = dalloc(&o, (size_t)chunk_rows * l->M);
+    if (st == MDN_OK) st = dalloc(&c, (size_t)chunk_rows * ((m->C + 1) / 2));
     x->dA.push_back(a);
     x->dOut.push_back(o);
+    x->dC.push_back(c);
     if (st != MDN_OK) {
       mdn_exec_free(x.release());
       return st;
@@ -782,6 +787,71 @@ int mdn_amm_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* out
 int mdn_amm_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, float* out,
                     int64_t ldo) {
   return amm_host<uint8_t>(x, A, N, lda, out, ldo);
+}
+
+// Unfused halves through host buffers: g (host A -> host codes) and f (host
+// codes -> host out) on the same slots and streams (codes in the slot's code
+// buffer).
+int mdn_encode_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes) {
+  if (!x || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  const int D = x->model->D;
+  const int64_t nb = (x->model->C + 1) / 2;
+  if (!A || !codes || lda < D) return MDN_EINVAL;
+  DeviceGuard g(x->device);
+  if (!g.ok) return MDN_ECUDA;
+  cudaError_t e = cudaSuccess;
+  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
+  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
+    const int s = (int)(q % x->n_slots);
+    cudaStream_t st = x->streams[s];
+    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
+    float* dA = x->dA[s];
+    uint8_t* dC = x->dC[s];
+    e = lda == D ? cudaMemcpyAsync(dA, A + r0 * lda, (size_t)n * D * sizeof(float), cudaMemcpyHostToDevice, st)
+                 : cudaMemcpy2DAsync(dA, D * sizeof(float), A + r0 * lda, lda * sizeof(float),
+                                     D * sizeof(float), n, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) break;
+    e = launch_encode(x->model->trees(), dA, n, D, dC, st);
+    if (e != cudaSuccess) break;
+    e = cudaMemcpyAsync(codes + r0 * nb, dC, (size_t)n * nb, cudaMemcpyDeviceToHost, st);
+  }
+  for (auto s : x->streams) {
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+  }
+  return cuda_status(e);
+}
+
+int mdn_scan_host(mdn_exec* x, const uint8_t* codes, int64_t N, float* out, int64_t ldo) {
+  if (!x || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  const int M = x->luts->M;
+  const int64_t nb = (x->model->C + 1) / 2;
+  if (!codes || !out || ldo < M) return MDN_EINVAL;
+  DeviceGuard g(x->device);
+  if (!g.ok) return MDN_ECUDA;
+  cudaError_t e = cudaSuccess;
+  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
+  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
+    const int s = (int)(q % x->n_slots);
+    cudaStream_t st = x->streams[s];
+    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
+    uint8_t* dC = x->dC[s];
+    e = cudaMemcpyAsync(dC, codes + r0 * nb, (size_t)n * nb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) break;
+    e = launch_scan(x->luts->dev(), dC, n, nullptr, x->dOut[s], M, st);
+    if (e != cudaSuccess) break;
+    e = ldo == M ? cudaMemcpyAsync(out + r0 * ldo, x->dOut[s], (size_t)n * M * sizeof(float),
+                                   cudaMemcpyDeviceToHost, st)
+                 : cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
+                                     M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
+  }
+  for (auto s : x->streams) {
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+  }
+  return cuda_status(e);
 }
 
 // Column-major host A: per chunk only the distinct split columns

@@ -313,3 +313,26 @@ def test_scan_strided_out(mdn, name, layout):
     rest = raw.clone()
     rest[off:off + n * ldo].view(n, ldo)[:, :M] = 0
     assert torch.isnan(rest[rest != 0]).all()
+
+
+@pytest.mark.parametrize("name,chunk", [("cls100", 1536), ("tiny", 1000), ("image", 4096)])
+def test_host_encode_and_scan(mdn, name, chunk):
+    """mdn_encode_host / mdn_scan_host: the unfused halves through the
+    pipelined host-buffer executor, ragged last chunk, strided host rows."""
+    model, om, A, B = _setup(mdn, name)
+    A = A[:5003]
+    N = A.shape[0]
+    spec = CONFIGS[name]
+    luts = mdn.mdn_build_luts(model, B, 0)
+    codes_o, _, want = O.amm(A, om, O.make_luts(om, B, "exact"))
+    ex = mdn.mdn_exec_create(model, luts, chunk_rows=chunk, n_slots=3)
+    A_h = torch.zeros((N, spec.D + 4)).pin_memory()
+    A_h[:, :spec.D] = torch.from_numpy(A)
+    c_h = torch.empty((N, (spec.C + 1) // 2), dtype=torch.uint8).pin_memory()
+    mdn.mdn_encode_host(ex, A_h[:, :spec.D], c_h)
+    assert (c_h.numpy() == O.pack_codes(codes_o)).all()
+    out_h = torch.full((N, spec.M + 1), float("nan")).pin_memory()
+    mdn.mdn_scan_host(ex, torch.from_numpy(O.pack_codes(codes_o)), out_h[:, :spec.M])
+    ex.close()
+    _assert_out(out_h[:, :spec.M].numpy(), want)
+    assert torch.isnan(out_h[:, spec.M:]).all()
