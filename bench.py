@@ -259,6 +259,18 @@ def run_train(args):
         blob = mdn.mdn_train(A, spec.C, 1.0)                 # synchronous
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
+    # End to end from host memory: the training split's host->device copy
+    # (pageable numpy rows, as a user hands them over) + the call, whose
+    # model bytes come back to the host.
+    e2e_times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        blob = mdn.mdn_train(torch.from_numpy(A_h).cuda(), spec.C, 1.0)
+        e2e_times.append(time.perf_counter() - t0)
+    t_e2e = statistics.median(e2e_times)
+    e2e = {"value": A_h.shape[0] / t_e2e, "unit": "rows/s", "h2d_bytes_per_step": int(A_h.nbytes),
+           "d2h_bytes_per_step": len(blob), "steps": args.steps,
+           "path": "host rows -> device (torch copy) + mdn_train (model bytes returned to the host)"}
     # Kernel launches of one training call, counted by the CUDA profiler on an
     # extra untimed call: the library's own kernels (namespace mdn) and the
     # library-routine kernels it calls (CUB segmented sort, cuSOLVER).
@@ -301,7 +313,7 @@ def run_train(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{name} training split, trees + ridge prototypes (lambda = 1)",
                        "rows": int(A_h.shape[0])},
-            "roofline": None, "cpu_baseline": cpu, "e2e": None,
+            "roofline": None, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": (launches["ours_per_call"] * args.steps
                              if launches and "ours_per_call" in launches else None),
             "launches_per_call": launches,
