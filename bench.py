@@ -561,17 +561,18 @@ def run(args):
                + " (pinned host A -> 3-slot pipelined H2D/kernel/D2H)"}
         ex.close()
         del A_h, out_h
-    elif op in ("encode", "scan") and not col and not pq and not u8 and (rank == 0 or ws > 1):
+    elif op in ("encode", "scan") and not col and not pq and (rank == 0 or ws > 1):
         # the unfused halves through host buffers (mdn_encode_host / mdn_scan_host)
         nb = (spec.C + 1) // 2
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
                                  n_slots=3)
-        n_e2e = min(n, (1 << 30) // (4 * spec.D))
+        n_e2e = min(n, (1 << 30) // (ea * spec.D))
         if op == "encode":
             A_h = A[:n_e2e].cpu().pin_memory()
             c_h = torch.empty((n_e2e, nb), dtype=torch.uint8).pin_memory()
-            host_call = lambda: mdn.mdn_encode_host(ex, A_h, c_h)
-            h2d, d2h = n_e2e * 4 * spec.D, n_e2e * nb
+            enc_host = mdn.mdn_encode_host_u8 if u8 else mdn.mdn_encode_host
+            host_call = lambda: enc_host(ex, A_h, c_h)
+            h2d, d2h = n_e2e * ea * spec.D, n_e2e * nb
         else:
             c_h = codes[:n_e2e].cpu().pin_memory()
             A_h = torch.empty((n_e2e, spec.M), dtype=torch.float32).pin_memory()   # out
@@ -588,7 +589,8 @@ def run(args):
         e2e = {"value": n_e2e * ws * e2e_steps / t_e2e, "unit": "rows/s",
                "rows_per_step": n_e2e * ws, "h2d_bytes_per_step": h2d * ws,
                "d2h_bytes_per_step": d2h * ws, "steps": e2e_steps,
-               "path": f"mdn_{op}_host (pinned host buffers -> 3-slot pipelined H2D/kernel/D2H)"}
+               "path": f"mdn_{op}_host{'_u8' if u8 and op == 'encode' else ''} (pinned host buffers -> "
+                       "3-slot pipelined H2D/kernel/D2H)"}
         ex.close()
         del A_h, c_h
     elif op == "amm" and col and not pq and (rank == 0 or ws > 1):

@@ -226,6 +226,9 @@ int mdn_encode_host(mdn_exec* exec, const float* A_host, int64_t N, int64_t lda,
                     uint8_t* codes_host);
 int mdn_scan_host(mdn_exec* exec, const uint8_t* codes_host, int64_t N, float* out_host,
                   int64_t ldo);
+/* g on natively 8-bit host rows (mdn_encode_u8), lda in bytes. */
+int mdn_encode_host_u8(mdn_exec* exec, const uint8_t* A_host, int64_t N, int64_t lda,
+                       uint8_t* codes_host);
 /* The same pipeline for column-major host A (mdn_amm_cm; SURVEY N2, P:L246,
  * P:L431): At_host fp32 D x N, row stride ldt >= N (column n of A = row n of
  * the result). Per chunk only the model's distinct split columns of At are

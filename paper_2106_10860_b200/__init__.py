@@ -62,6 +62,7 @@ _SIGS = {
     "mdn_amm_cm_host": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64]),
     "mdn_encode_host": (_i32, [_vp, _vp, _i64, _i64, _vp]),
     "mdn_scan_host": (_i32, [_vp, _vp, _i64, _vp, _i64]),
+    "mdn_encode_host_u8": (_i32, [_vp, _vp, _i64, _i64, _vp]),
     "mdn_train": (_i32, [_vp, _i64, _i64, _i32, _i32, ct.c_double, _i32, _vp, ct.POINTER(_sz)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -379,6 +380,24 @@ def mdn_encode_host(ex: Exec, A_host, codes_host):
     if sc != (sa[0], (ex._model.C + 1) // 2):
         raise ValueError("codes_host must be N x ceil(C/2)")
     _check(_lib.mdn_encode_host(ex._h, pa, sa[0], lda, pc), "mdn_encode_host")
+    return codes_host
+
+
+def mdn_encode_host_u8(ex: Exec, A_host, codes_host):
+    """g on 8-bit host rows through the executor."""
+    import torch
+    if isinstance(A_host, np.ndarray) and A_host.dtype == np.uint8 and A_host.ndim == 2 \
+            and A_host.strides[1] == 1:
+        pa, lda, sa = A_host.ctypes.data, A_host.strides[0], A_host.shape
+    elif isinstance(A_host, torch.Tensor) and not A_host.is_cuda and A_host.dtype == torch.uint8 \
+            and A_host.dim() == 2 and A_host.stride(1) == 1:
+        pa, lda, sa = A_host.data_ptr(), A_host.stride(0), tuple(A_host.shape)
+    else:
+        raise TypeError("A_host must be host uint8 (numpy or CPU tensor)")
+    pc, sc = _host_u8(codes_host, "codes_host")
+    if sc != (sa[0], (ex._model.C + 1) // 2):
+        raise ValueError("codes_host must be N x ceil(C/2)")
+    _check(_lib.mdn_encode_host_u8(ex._h, pa, sa[0], lda, pc), "mdn_encode_host_u8")
     return codes_host
 
 

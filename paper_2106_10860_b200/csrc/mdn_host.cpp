@@ -792,7 +792,11 @@ int mdn_amm_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, float
 // Unfused halves through host buffers: g (host A -> host codes) and f (host
 // codes -> host out) on the same slots and streams (codes in the slot's code
 // buffer).
-int mdn_encode_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes) {
+}  // extern "C"
+
+namespace {
+template <class TIn>
+int encode_host(mdn_exec* x, const TIn* A, int64_t N, int64_t lda, uint8_t* codes) {
   if (!x || N < 0) return MDN_EINVAL;
   if (N == 0) return MDN_OK;
   const int D = x->model->D;
@@ -806,13 +810,16 @@ int mdn_encode_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t
     const int s = (int)(q % x->n_slots);
     cudaStream_t st = x->streams[s];
     const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
-    float* dA = x->dA[s];
+    TIn* dA = reinterpret_cast<TIn*>(x->dA[s]);          // sized for fp32 rows
     uint8_t* dC = x->dC[s];
-    e = lda == D ? cudaMemcpyAsync(dA, A + r0 * lda, (size_t)n * D * sizeof(float), cudaMemcpyHostToDevice, st)
-                 : cudaMemcpy2DAsync(dA, D * sizeof(float), A + r0 * lda, lda * sizeof(float),
-                                     D * sizeof(float), n, cudaMemcpyHostToDevice, st);
+    e = lda == D ? cudaMemcpyAsync(dA, A + r0 * lda, (size_t)n * D * sizeof(TIn), cudaMemcpyHostToDevice, st)
+                 : cudaMemcpy2DAsync(dA, D * sizeof(TIn), A + r0 * lda, lda * sizeof(TIn),
+                                     D * sizeof(TIn), n, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) break;
-    e = launch_encode(x->model->trees(), dA, n, D, dC, st);
+    if constexpr (sizeof(TIn) == 1)
+      e = launch_encode_u8(x->model->trees(), dA, n, D, dC, st);
+    else
+      e = launch_encode(x->model->trees(), dA, n, D, dC, st);
     if (e != cudaSuccess) break;
     e = cudaMemcpyAsync(codes + r0 * nb, dC, (size_t)n * nb, cudaMemcpyDeviceToHost, st);
   }
@@ -821,6 +828,17 @@ int mdn_encode_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t
     if (e == cudaSuccess) e = e2;
   }
   return cuda_status(e);
+}
+}  // namespace
+
+extern "C" {
+
+int mdn_encode_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes) {
+  return encode_host<float>(x, A, N, lda, codes);
+}
+
+int mdn_encode_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, uint8_t* codes) {
+  return encode_host<uint8_t>(x, A, N, lda, codes);
 }
 
 int mdn_scan_host(mdn_exec* x, const uint8_t* codes, int64_t N, float* out, int64_t ldo) {

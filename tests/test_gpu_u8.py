@@ -93,3 +93,6 @@ def test_u8_host_executor(mdn):
     out_h = torch.empty((A.shape[0], 2)).pin_memory()
     mdn.mdn_amm_host_u8(ex, A_h, out_h)
     assert (out_h.numpy().view(np.uint32) == want.view(np.uint32)).all()
+    codes_h = torch.empty((A.shape[0], 4), dtype=torch.uint8).pin_memory()
+    mdn.mdn_encode_host_u8(ex, A_h, codes_h)                     # g on host 8-bit rows
+    assert (codes_h.numpy() == O.pack_codes(O.encode_u8(A, om))).all()
