@@ -593,26 +593,33 @@ def run(args):
                        "3-slot pipelined H2D/kernel/D2H)"}
         ex.close()
         del A_h, c_h
-    elif op == "amm" and col and not pq and (rank == 0 or ws > 1):
+    elif op in ("amm", "encode") and col and not pq and (rank == 0 or ws > 1):
         # column-major host A: only the split columns cross PCIe (N2)
         ex = mdn.mdn_exec_create(model, luts, chunk_rows=1 << 18, n_slots=3)
         n_e2e = min(n, (1 << 30) // (4 * spec.D))
         At_h = A[:, :n_e2e].contiguous().cpu().pin_memory()          # A is At (D x n) here
-        out_h = torch.empty((n_e2e, spec.M), dtype=torch.float32).pin_memory()
-        mdn.mdn_amm_cm_host(ex, At_h, out_h)                  # warm-up
+        if op == "amm":
+            out_h = torch.empty((n_e2e, spec.M), dtype=torch.float32).pin_memory()
+            host_call = lambda: mdn.mdn_amm_cm_host(ex, At_h, out_h)
+            d2h = n_e2e * 4 * spec.M
+        else:
+            out_h = torch.empty((n_e2e, (spec.C + 1) // 2), dtype=torch.uint8).pin_memory()
+            host_call = lambda: mdn.mdn_encode_cm_host(ex, At_h, out_h)
+            d2h = n_e2e * ((spec.C + 1) // 2)
+        host_call()                                           # warm-up
         e2e_steps = max(1, min(args.steps, 3))
         if ws > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            mdn.mdn_amm_cm_host(ex, At_h, out_h)
+            host_call()
         t_e2e = allreduce_max(time.perf_counter() - t0)
         e2e = {"value": n_e2e * ws * e2e_steps / t_e2e, "unit": "rows/s",
                "rows_per_step": n_e2e * ws,
                "h2d_bytes_per_step": n_e2e * 4 * len(split_dims(model_blob)) * ws,
-               "d2h_bytes_per_step": n_e2e * 4 * spec.M * ws,
+               "d2h_bytes_per_step": d2h * ws,
                "steps": e2e_steps,
-               "path": "mdn_amm_cm_host (pinned column-major host A, split columns only -> "
+               "path": f"mdn_{op}_cm_host (pinned column-major host A, split columns only -> "
                        "3-slot pipelined H2D/kernel/D2H)"}
         ex.close()
         del At_h, out_h

@@ -237,6 +237,10 @@ int mdn_encode_host_u8(mdn_exec* exec, const uint8_t* A_host, int64_t N, int64_t
  * mdn_amm_host; ldt < N -> MDN_EINVAL. */
 int mdn_amm_cm_host(mdn_exec* exec, const float* At_host, int64_t N, int64_t ldt,
                     float* out_host, int64_t ldo);
+/* g on column-major host A: split columns in, packed codes (N x ceil(C/2),
+ * contiguous host u8) out. */
+int mdn_encode_cm_host(mdn_exec* exec, const float* At_host, int64_t N, int64_t ldt,
+                       uint8_t* codes_host);
 
 /* --------------------------------------------------------- diagnostics -- */
 

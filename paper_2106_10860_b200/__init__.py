@@ -63,6 +63,7 @@ _SIGS = {
     "mdn_encode_host": (_i32, [_vp, _vp, _i64, _i64, _vp]),
     "mdn_scan_host": (_i32, [_vp, _vp, _i64, _vp, _i64]),
     "mdn_encode_host_u8": (_i32, [_vp, _vp, _i64, _i64, _vp]),
+    "mdn_encode_cm_host": (_i32, [_vp, _vp, _i64, _i64, _vp]),
     "mdn_train": (_i32, [_vp, _i64, _i64, _i32, _i32, ct.c_double, _i32, _vp, ct.POINTER(_sz)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -423,6 +424,18 @@ def mdn_amm_cm_host(ex: Exec, At_host, out_host):
         raise ValueError("row count mismatch")
     _check(_lib.mdn_amm_cm_host(ex._h, pa, sa[1], ldt, po, ldo), "mdn_amm_cm_host")
     return out_host
+
+
+def mdn_encode_cm_host(ex: Exec, At_host, codes_host):
+    """g on column-major host A through the executor (split columns only)."""
+    pa, ldt, sa = _host_ptr(At_host, "At_host")
+    pc, sc = _host_u8(codes_host, "codes_host")
+    if sa[0] != ex._model.D:
+        raise ValueError("At_host must be D x N")
+    if sc != (sa[1], (ex._model.C + 1) // 2):
+        raise ValueError("codes_host must be N x ceil(C/2)")
+    _check(_lib.mdn_encode_cm_host(ex._h, pa, sa[1], ldt, pc), "mdn_encode_cm_host")
+    return codes_host
 
 
 def mdn_stream_probe(A, out, stream=None):

@@ -872,6 +872,53 @@ int mdn_scan_host(mdn_exec* x, const uint8_t* codes, int64_t N, float* out, int6
   return cuda_status(e);
 }
 
+namespace {
+// Copy chunk [r0, r0 + n) of the split columns of host At (D x N, ldt) into
+// the slot's D x chunk column-major tile; adjacent columns as one 2-D copy.
+cudaError_t copy_split_columns(const mdn_exec* x, float* dAt, const float* At, int64_t ldt,
+                               int64_t r0, int64_t n, cudaStream_t st) {
+  const std::vector<uint16_t>& cols = x->model->h_cols;
+  cudaError_t e = cudaSuccess;
+  for (size_t i = 0; i < cols.size() && e == cudaSuccess;) {
+    size_t j = i + 1;
+    while (j < cols.size() && cols[j] == cols[j - 1] + 1) ++j;
+    const int64_t c0 = cols[i];
+    e = cudaMemcpy2DAsync(dAt + c0 * x->chunk, (size_t)x->chunk * sizeof(float),
+                          At + c0 * ldt + r0, (size_t)ldt * sizeof(float),
+                          (size_t)n * sizeof(float), j - i, cudaMemcpyHostToDevice, st);
+    i = j;
+  }
+  return e;
+}
+}  // namespace
+
+// g on column-major host A: split columns in, packed codes out.
+int mdn_encode_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, uint8_t* codes) {
+  if (!x || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!At || !codes || ldt < N) return MDN_EINVAL;
+  DeviceGuard g(x->device);
+  if (!g.ok) return MDN_ECUDA;
+  const int64_t nb = (x->model->C + 1) / 2;
+  cudaError_t e = cudaSuccess;
+  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
+  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
+    const int s = (int)(q % x->n_slots);
+    cudaStream_t st = x->streams[s];
+    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
+    e = copy_split_columns(x, x->dA[s], At, ldt, r0, n, st);
+    if (e != cudaSuccess) break;
+    e = launch_encode_cm(x->model->trees(), x->dA[s], n, x->chunk, x->dC[s], st);
+    if (e != cudaSuccess) break;
+    e = cudaMemcpyAsync(codes + r0 * nb, x->dC[s], (size_t)n * nb, cudaMemcpyDeviceToHost, st);
+  }
+  for (auto s : x->streams) {
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+  }
+  return cuda_status(e);
+}
+
 // Column-major host A: per chunk only the distinct split columns
 // cross PCIe (4 |S| instead of 4 D bytes per row). The slot buffer is used as
 // a D x chunk column-major tile (ldt = chunk); rows of At that are not split
@@ -885,7 +932,6 @@ int mdn_amm_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, float*
   if (!At || !out || ldt < N || ldo < M) return MDN_EINVAL;
   DeviceGuard g(x->device);
   if (!g.ok) return MDN_ECUDA;
-  const std::vector<uint16_t>& cols = x->model->h_cols;
   cudaError_t e = cudaSuccess;
   const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
   for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
@@ -893,15 +939,7 @@ int mdn_amm_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, float*
     cudaStream_t st = x->streams[s];
     const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
     float* dAt = x->dA[s];
-    for (size_t i = 0; i < cols.size() && e == cudaSuccess;) {
-      size_t j = i + 1;
-      while (j < cols.size() && cols[j] == cols[j - 1] + 1) ++j;     // run of adjacent columns
-      const int64_t c0 = cols[i];
-      e = cudaMemcpy2DAsync(dAt + c0 * x->chunk, (size_t)x->chunk * sizeof(float),
-                            At + c0 * ldt + r0, (size_t)ldt * sizeof(float),
-                            (size_t)n * sizeof(float), j - i, cudaMemcpyHostToDevice, st);
-      i = j;
-    }
+    e = copy_split_columns(x, dAt, At, ldt, r0, n, st);
     if (e != cudaSuccess) break;
     e = launch_amm_cm(x->model->trees(), x->luts->dev(), dAt, n, x->chunk, x->dOut[s], M, st);
     if (e != cudaSuccess) break;

@@ -193,6 +193,9 @@ def test_cm_host_executor(mdn, name, chunk):
     out_h = torch.full((N, spec.M + 3), float("nan")).pin_memory()
     ex = mdn.mdn_exec_create(model, luts, chunk_rows=chunk, n_slots=3)
     mdn.mdn_amm_cm_host(ex, At_h[:, :N], out_h[:, :spec.M])
+    codes_h = torch.empty((N, (spec.C + 1) // 2), dtype=torch.uint8).pin_memory()
+    mdn.mdn_encode_cm_host(ex, At_h[:, :N], codes_h)
+    assert (codes_h.numpy() == O.pack_codes(O.encode(A, om))).all()
     ex.close()
     _assert_out(out_h[:, :spec.M].numpy(), want)
     assert torch.isnan(out_h[:, spec.M:]).all()
