@@ -561,6 +561,34 @@ def run(args):
                + " (pinned host A -> 3-slot pipelined H2D/kernel/D2H)"}
         ex.close()
         del A_h, out_h
+    elif op in ("amm", "encode") and pq and (rank == 0 or ws > 1):
+        # the PQ comparator through host buffers (mdn_amm_pq_host / mdn_encode_pq_host)
+        ex = mdn.mdn_exec_create(model, luts, chunk_rows=max(1 << 12, (1 << 28) // (4 * spec.D)),
+                                 n_slots=3)
+        n_e2e = min(n, (1 << 30) // (4 * spec.D))
+        A_h = A[:n_e2e].cpu().pin_memory()
+        if op == "amm":
+            o_h = torch.empty((n_e2e, spec.M), dtype=torch.float32).pin_memory()
+            host_call = lambda: mdn.mdn_amm_pq_host(ex, A_h, o_h)
+            d2h = n_e2e * 4 * spec.M
+        else:
+            o_h = torch.empty((n_e2e, (spec.C + 1) // 2), dtype=torch.uint8).pin_memory()
+            host_call = lambda: mdn.mdn_encode_pq_host(ex, A_h, o_h)
+            d2h = n_e2e * ((spec.C + 1) // 2)
+        host_call()                                           # warm-up
+        e2e_steps = max(1, min(args.steps, 3))
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            host_call()
+        t_e2e = allreduce_max(time.perf_counter() - t0)
+        e2e = {"value": n_e2e * ws * e2e_steps / t_e2e, "unit": "rows/s",
+               "rows_per_step": n_e2e * ws, "h2d_bytes_per_step": n_e2e * 4 * spec.D * ws,
+               "d2h_bytes_per_step": d2h * ws, "steps": e2e_steps,
+               "path": f"mdn_{op}_pq_host (pinned host rows -> 3-slot pipelined H2D/kernel/D2H)"}
+        ex.close()
+        del A_h, o_h
     elif op in ("encode", "scan") and not col and not pq and (rank == 0 or ws > 1):
         # the unfused halves through host buffers (mdn_encode_host / mdn_scan_host)
         nb = (spec.C + 1) // 2

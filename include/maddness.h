@@ -237,6 +237,15 @@ int mdn_encode_host_u8(mdn_exec* exec, const uint8_t* A_host, int64_t N, int64_t
  * mdn_amm_host; ldt < N -> MDN_EINVAL. */
 int mdn_amm_cm_host(mdn_exec* exec, const float* At_host, int64_t N, int64_t ldt,
                     float* out_host, int64_t ldo);
+/* The PQ comparator through the same executor, which must have
+ * been created with a PQ model: host rows -> host codes (mdn_encode_pq), or
+ * host rows -> host out (mdn_encode_pq + mdn_scan per chunk on the device).
+ * The tree-based host calls return MDN_ESTATE for a PQ executor and these
+ * two for a MADDNESS one. */
+int mdn_encode_pq_host(mdn_exec* exec, const float* A_host, int64_t N, int64_t lda,
+                       uint8_t* codes_host);
+int mdn_amm_pq_host(mdn_exec* exec, const float* A_host, int64_t N, int64_t lda,
+                    float* out_host, int64_t ldo);
 /* g on column-major host A: split columns in, packed codes (N x ceil(C/2),
  * contiguous host u8) out. */
 int mdn_encode_cm_host(mdn_exec* exec, const float* At_host, int64_t N, int64_t ldt,

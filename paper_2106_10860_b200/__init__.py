@@ -64,6 +64,8 @@ _SIGS = {
     "mdn_scan_host": (_i32, [_vp, _vp, _i64, _vp, _i64]),
     "mdn_encode_host_u8": (_i32, [_vp, _vp, _i64, _i64, _vp]),
     "mdn_encode_cm_host": (_i32, [_vp, _vp, _i64, _i64, _vp]),
+    "mdn_encode_pq_host": (_i32, [_vp, _vp, _i64, _i64, _vp]),
+    "mdn_amm_pq_host": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64]),
     "mdn_train": (_i32, [_vp, _i64, _i64, _i32, _i32, ct.c_double, _i32, _vp, ct.POINTER(_sz)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -436,6 +438,26 @@ def mdn_encode_cm_host(ex: Exec, At_host, codes_host):
         raise ValueError("codes_host must be N x ceil(C/2)")
     _check(_lib.mdn_encode_cm_host(ex._h, pa, sa[1], ldt, pc), "mdn_encode_cm_host")
     return codes_host
+
+
+def mdn_encode_pq_host(ex: Exec, A_host, codes_host):
+    """PQ encode of host rows through a PQ executor."""
+    pa, lda, sa = _host_ptr(A_host, "A_host")
+    pc, sc = _host_u8(codes_host, "codes_host")
+    if sc != (sa[0], (ex._model.C + 1) // 2):
+        raise ValueError("codes_host must be N x ceil(C/2)")
+    _check(_lib.mdn_encode_pq_host(ex._h, pa, sa[0], lda, pc), "mdn_encode_pq_host")
+    return codes_host
+
+
+def mdn_amm_pq_host(ex: Exec, A_host, out_host):
+    """PQ encode + scan + dequant of host rows through a PQ executor."""
+    pa, lda, sa = _host_ptr(A_host, "A_host")
+    po, ldo, so = _host_ptr(out_host, "out_host")
+    if so[0] != sa[0]:
+        raise ValueError("row count mismatch")
+    _check(_lib.mdn_amm_pq_host(ex._h, pa, sa[0], lda, po, ldo), "mdn_amm_pq_host")
+    return out_host
 
 
 def mdn_stream_probe(A, out, stream=None):

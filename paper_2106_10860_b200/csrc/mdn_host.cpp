@@ -698,7 +698,7 @@ int mdn_exec_create(const mdn_model* m, const mdn_luts* l, int64_t chunk_rows, i
                     mdn_exec** out) {
   if (!m || !l || !out || chunk_rows < 1 || n_slots < 1 || n_slots > 8) return MDN_EINVAL;
   if (l->C != m->C) return MDN_ESHAPE;
-  if (l->model_fp != m->fingerprint || m->pq) return MDN_ESTATE;
+  if (l->model_fp != m->fingerprint) return MDN_ESTATE;
   *out = nullptr;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
@@ -741,6 +741,7 @@ namespace {
 template <class TIn>
 int amm_host(mdn_exec* x, const TIn* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
   if (!x || N < 0) return MDN_EINVAL;
+  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_*_pq_host
   if (N == 0) return MDN_OK;
   const int D = x->model->D, M = x->luts->M;
   if (!A || !out || lda < D || ldo < M) return MDN_EINVAL;
@@ -798,6 +799,7 @@ namespace {
 template <class TIn>
 int encode_host(mdn_exec* x, const TIn* A, int64_t N, int64_t lda, uint8_t* codes) {
   if (!x || N < 0) return MDN_EINVAL;
+  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_*_pq_host
   if (N == 0) return MDN_OK;
   const int D = x->model->D;
   const int64_t nb = (x->model->C + 1) / 2;
@@ -895,6 +897,7 @@ cudaError_t copy_split_columns(const mdn_exec* x, float* dAt, const float* At, i
 // g on column-major host A: split columns in, packed codes out.
 int mdn_encode_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, uint8_t* codes) {
   if (!x || N < 0) return MDN_EINVAL;
+  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_*_pq_host
   if (N == 0) return MDN_OK;
   if (!At || !codes || ldt < N) return MDN_EINVAL;
   DeviceGuard g(x->device);
@@ -919,6 +922,60 @@ int mdn_encode_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, uin
   return cuda_status(e);
 }
 
+// PQ comparator through host buffers: codes only (out == null)
+// or codes + scan + dequant per chunk on the device (the two-launch PQ amm).
+static int pq_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes,
+                   float* out, int64_t ldo) {
+  if (!x || N < 0) return MDN_EINVAL;
+  const mdn_model* m = x->model;
+  if (!m->pq) return MDN_ESTATE;
+  if (N == 0) return MDN_OK;
+  const int D = m->D, M = x->luts->M;
+  const int64_t nb = (m->C + 1) / 2;
+  if (!A || lda < D || (!codes && !out) || (out && ldo < M)) return MDN_EINVAL;
+  DeviceGuard g(x->device);
+  if (!g.ok) return MDN_ECUDA;
+  cudaError_t e = cudaSuccess;
+  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
+  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
+    const int s = (int)(q % x->n_slots);
+    cudaStream_t st = x->streams[s];
+    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
+    float* dA = x->dA[s];
+    e = lda == D ? cudaMemcpyAsync(dA, A + r0 * lda, (size_t)n * D * sizeof(float), cudaMemcpyHostToDevice, st)
+                 : cudaMemcpy2DAsync(dA, D * sizeof(float), A + r0 * lda, lda * sizeof(float),
+                                     D * sizeof(float), n, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) break;
+    e = launch_encode_pq(m->trees(), m->d_P, m->d_sub, m->d_sub_e, dA, n, D, x->dC[s], st);
+    if (e != cudaSuccess) break;
+    if (out) {
+      e = launch_scan(x->luts->dev(), x->dC[s], n, nullptr, x->dOut[s], M, st);
+      if (e != cudaSuccess) break;
+      e = ldo == M ? cudaMemcpyAsync(out + r0 * ldo, x->dOut[s], (size_t)n * M * sizeof(float),
+                                     cudaMemcpyDeviceToHost, st)
+                   : cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
+                                       M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
+    } else {
+      e = cudaMemcpyAsync(codes + r0 * nb, x->dC[s], (size_t)n * nb, cudaMemcpyDeviceToHost, st);
+    }
+  }
+  for (auto s : x->streams) {
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+  }
+  return cuda_status(e);
+}
+
+int mdn_encode_pq_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes) {
+  if (!codes) return MDN_EINVAL;
+  return pq_host(x, A, N, lda, codes, nullptr, 0);
+}
+
+int mdn_amm_pq_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
+  if (!out) return MDN_EINVAL;
+  return pq_host(x, A, N, lda, nullptr, out, ldo);
+}
+
 // Column-major host A: per chunk only the distinct split columns
 // cross PCIe (4 |S| instead of 4 D bytes per row). The slot buffer is used as
 // a D x chunk column-major tile (ldt = chunk); rows of At that are not split
@@ -927,6 +984,7 @@ int mdn_encode_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, uin
 int mdn_amm_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, float* out,
                     int64_t ldo) {
   if (!x || N < 0) return MDN_EINVAL;
+  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_*_pq_host
   if (N == 0) return MDN_OK;
   const int M = x->luts->M;
   if (!At || !out || ldt < N || ldo < M) return MDN_EINVAL;

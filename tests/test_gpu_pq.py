@@ -117,3 +117,34 @@ def test_encode_pq_bench_size_sampled(mdn, base):
     assert (got == want).all(), f"{(got != want).sum()} code bytes differ"
     del A, codes
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("base", ["tiny", "cls100"])
+def test_pq_host_executor(mdn, base):
+    """mdn_encode_pq_host / mdn_amm_pq_host through a PQ executor (ragged last
+    chunk, strided host rows) equal the oracle; the tree-based host calls
+    refuse the PQ executor and the PQ calls a MADDNESS one (MDN_ESTATE)."""
+    model, om, A, B = _setup(mdn, base)
+    A = A[:3001]
+    N, D = A.shape
+    luts = mdn.mdn_build_luts(model, B, 1, CONFIGS[base].U)
+    codes_o, _, want = O.amm_pq(A, om, O.make_luts(om, B, "avg", CONFIGS[base].U))
+    ex = mdn.mdn_exec_create(model, luts, chunk_rows=1000, n_slots=3)
+    A_h = torch.zeros((N, D + 4)).pin_memory()
+    A_h[:, :D] = torch.from_numpy(A)
+    c_h = torch.empty((N, om.C // 2), dtype=torch.uint8).pin_memory()
+    mdn.mdn_encode_pq_host(ex, A_h[:, :D], c_h)
+    assert (c_h.numpy() == O.pack_codes(codes_o)).all()
+    out_h = torch.empty((N, B.shape[1])).pin_memory()
+    mdn.mdn_amm_pq_host(ex, A_h[:, :D], out_h)
+    _assert_out(out_h.numpy(), want)
+    with pytest.raises(mdn.MdnError) as e:
+        mdn.mdn_amm_host(ex, A_h[:, :D], torch.empty((N, B.shape[1])))
+    assert e.value.status == -5
+    ex.close()
+    mdd = mdn.mdn_model_load(model_bytes(base), 0)
+    ex2 = mdn.mdn_exec_create(mdd, mdn.mdn_build_luts(mdd, B, 0), chunk_rows=1000, n_slots=2)
+    with pytest.raises(mdn.MdnError) as e:
+        mdn.mdn_encode_pq_host(ex2, A_h[:, :D], c_h)
+    assert e.value.status == -5
+    ex2.close()
