@@ -9,16 +9,19 @@
 // HBM bytes per row are 4 |S| + 4M (|S| = distinct split dims) instead of
 // 4D + 4M: 912 vs 2448 for the CIFAR-100-shaped config.
 //
-// The fused path runs the warp-specialised TMA kernel of mdn_fast.cu with a
-// [slot][row] stage layout filled by TMA gather4 (launch_amm_ws_cm) whenever
-// its shapes are supported; the thread-per-row kernel here is the fallback
-// and the encode-only path.
+// For C >= 16 the fused path and the encoder run the warp-specialised TMA
+// kernel of mdn_fast.cu with a [slot][row] stage layout filled by TMA gather4
+// (launch_amm_ws_cm / launch_encode_ws_cm) whenever its shapes are
+// supported; the kernel here serves C <= 8 (tiny, image) and is the fallback.
 //
-// k_amm_cm: thread per row. For each group of 8 codebooks the 32 split values
-// are loaded (streaming, evict-first: each is used once), Algorithm 1 runs on
-// thresholds resident in shared memory, and the packed codes feed the same
-// shared-memory table scan as the row-major fused kernel (mdn_scan.cuh); the
-// codes never leave registers. ENC_ONLY writes the packed codes instead.
+// k_amm_cm: a thread owns RPT consecutive rows (4 for C = 4, 2 for C = 8 when
+// the columns are aligned for vector loads, else 1). For each group of 8
+// codebooks the split values are loaded (streaming, evict-first: each is used
+// once; one vector load per column covers the thread's rows), Algorithm 1
+// runs on thresholds resident in shared memory, and the packed codes feed the
+// same shared-memory table scan as the row-major fused kernel (mdn_scan.cuh);
+// the codes never leave registers. ENC_ONLY writes the packed codes instead
+// (one 8-byte store per thread when RPT rows of codes make 8 bytes).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
