@@ -32,6 +32,12 @@
 //     dequant     out = fl32(alpha_eff * S + beta32) (Eq. 1), S -> fp32
 //                 by the 2^23 magic-number trick (exact for S < 2^23), one
 //                 FFMA rounding; 8- or 16-byte stores.
+//
+// ENC (mdn_encode / mdn_encode_u8 for C in {4, 8}): the same producer and
+// encode, no tables and no scan; the C lanes of a row group hold a C x C
+// nibble matrix (rows x codebooks) which log2(C) rotate / shuffle / merge
+// stages transpose, so each lane ends with one row's packed codes and the
+// warp's 32 rows leave in one coalesced store.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
