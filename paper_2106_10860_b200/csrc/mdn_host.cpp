@@ -735,150 +735,56 @@ int mdn_exec_create(const mdn_model* m, const mdn_luts* l, int64_t chunk_rows, i
 
 }  // extern "C"
 
+// ------------------------------------------------ host-buffer pipelines --
+//
+// Every host call runs the same driver: chunk q of the rows goes through slot
+// q % n_slots on the slot's stream -- host->device copy, the device op, the
+// device->host copy -- so the copies of one chunk overlap the kernels of the
+// others; stream order serialises the reuse of a slot (chunk q's upload waits
+// for chunk q - n_slots' download). The per-op part is a chunk function.
 namespace {
-// Host-buffer pipeline shared by fp32 and 8-bit rows: chunk q goes H2D into
-// slot q % n_slots, through the fused kernel and back D2H on the slot's stream.
-template <class TIn>
-int amm_host(mdn_exec* x, const TIn* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
-  if (!x || N < 0) return MDN_EINVAL;
-  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_*_pq_host
-  if (N == 0) return MDN_OK;
-  const int D = x->model->D, M = x->luts->M;
-  if (!A || !out || lda < D || ldo < M) return MDN_EINVAL;
-  DeviceGuard g(x->device);
-  if (!g.ok) return MDN_ECUDA;
-  cudaError_t e = cudaSuccess;
-  int64_t nchunks = (N + x->chunk - 1) / x->chunk;
-  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
-    int s = (int)(q % x->n_slots);
-    cudaStream_t st = x->streams[s];
-    int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
-    TIn* dA = reinterpret_cast<TIn*>(x->dA[s]);        // sized for fp32 rows: 8-bit rows fit
-    // Stream order serialises reuse of slot s: H2D(q) waits for D2H(q - n_slots).
-    // Contiguous rows go as one linear copy: a 2-D copy of narrow rows (8-bit
-    // A, small M) runs row by row and far below the PCIe rate.
-    e = lda == D ? cudaMemcpyAsync(dA, A + r0 * lda, (size_t)n * D * sizeof(TIn), cudaMemcpyHostToDevice, st)
-                 : cudaMemcpy2DAsync(dA, D * sizeof(TIn), A + r0 * lda, lda * sizeof(TIn), D * sizeof(TIn),
-                                     n, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) break;
-    if constexpr (sizeof(TIn) == 1)
-      e = launch_amm_u8(x->model->trees(), x->luts->dev(), dA, n, D, x->dOut[s], M, st);
-    else
-      e = launch_amm(x->model->trees(), x->luts->dev(), dA, n, D, x->dOut[s], M, st);
-    if (e != cudaSuccess) break;
-    e = ldo == M ? cudaMemcpyAsync(out + r0 * ldo, x->dOut[s], (size_t)n * M * sizeof(float),
-                                   cudaMemcpyDeviceToHost, st)
-                 : cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
-                                     M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
-  }
-  for (auto s : x->streams) {
-    cudaError_t e2 = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) e = e2;
-  }
-  return cuda_status(e);
-}
-}  // namespace
 
-extern "C" {
-
-int mdn_amm_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
-  return amm_host<float>(x, A, N, lda, out, ldo);
-}
-
-int mdn_amm_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, float* out,
-                    int64_t ldo) {
-  return amm_host<uint8_t>(x, A, N, lda, out, ldo);
-}
-
-// Unfused halves through host buffers: g (host A -> host codes) and f (host
-// codes -> host out) on the same slots and streams (codes in the slot's code
-// buffer).
-}  // extern "C"
-
-namespace {
-template <class TIn>
-int encode_host(mdn_exec* x, const TIn* A, int64_t N, int64_t lda, uint8_t* codes) {
-  if (!x || N < 0) return MDN_EINVAL;
-  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_*_pq_host
-  if (N == 0) return MDN_OK;
-  const int D = x->model->D;
-  const int64_t nb = (x->model->C + 1) / 2;
-  if (!A || !codes || lda < D) return MDN_EINVAL;
+template <class ChunkFn>
+int run_pipeline(mdn_exec* x, int64_t N, ChunkFn&& chunk) {
   DeviceGuard g(x->device);
   if (!g.ok) return MDN_ECUDA;
   cudaError_t e = cudaSuccess;
   const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
   for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
     const int s = (int)(q % x->n_slots);
-    cudaStream_t st = x->streams[s];
     const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
-    TIn* dA = reinterpret_cast<TIn*>(x->dA[s]);          // sized for fp32 rows
-    uint8_t* dC = x->dC[s];
-    e = lda == D ? cudaMemcpyAsync(dA, A + r0 * lda, (size_t)n * D * sizeof(TIn), cudaMemcpyHostToDevice, st)
-                 : cudaMemcpy2DAsync(dA, D * sizeof(TIn), A + r0 * lda, lda * sizeof(TIn),
-                                     D * sizeof(TIn), n, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) break;
-    if constexpr (sizeof(TIn) == 1)
-      e = launch_encode_u8(x->model->trees(), dA, n, D, dC, st);
-    else
-      e = launch_encode(x->model->trees(), dA, n, D, dC, st);
-    if (e != cudaSuccess) break;
-    e = cudaMemcpyAsync(codes + r0 * nb, dC, (size_t)n * nb, cudaMemcpyDeviceToHost, st);
+    e = chunk(s, x->streams[s], r0, n);
   }
-  for (auto s : x->streams) {
-    cudaError_t e2 = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) e = e2;
-  }
-  return cuda_status(e);
-}
-}  // namespace
-
-extern "C" {
-
-int mdn_encode_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes) {
-  return encode_host<float>(x, A, N, lda, codes);
-}
-
-int mdn_encode_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, uint8_t* codes) {
-  return encode_host<uint8_t>(x, A, N, lda, codes);
-}
-
-int mdn_scan_host(mdn_exec* x, const uint8_t* codes, int64_t N, float* out, int64_t ldo) {
-  if (!x || N < 0) return MDN_EINVAL;
-  if (N == 0) return MDN_OK;
-  const int M = x->luts->M;
-  const int64_t nb = (x->model->C + 1) / 2;
-  if (!codes || !out || ldo < M) return MDN_EINVAL;
-  DeviceGuard g(x->device);
-  if (!g.ok) return MDN_ECUDA;
-  cudaError_t e = cudaSuccess;
-  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
-  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
-    const int s = (int)(q % x->n_slots);
-    cudaStream_t st = x->streams[s];
-    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
-    uint8_t* dC = x->dC[s];
-    e = cudaMemcpyAsync(dC, codes + r0 * nb, (size_t)n * nb, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) break;
-    e = launch_scan(x->luts->dev(), dC, n, nullptr, x->dOut[s], M, st);
-    if (e != cudaSuccess) break;
-    e = ldo == M ? cudaMemcpyAsync(out + r0 * ldo, x->dOut[s], (size_t)n * M * sizeof(float),
-                                   cudaMemcpyDeviceToHost, st)
-                 : cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
-                                     M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
-  }
-  for (auto s : x->streams) {
-    cudaError_t e2 = cudaStreamSynchronize(s);
+  for (auto st : x->streams) {
+    cudaError_t e2 = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = e2;
   }
   return cuda_status(e);
 }
 
-namespace {
-// Copy chunk [r0, r0 + n) of the split columns of host At (D x N, ldt) into
-// the slot's D x chunk column-major tile; adjacent columns as one 2-D copy.
-cudaError_t copy_split_columns(const mdn_exec* x, float* dAt, const float* At, int64_t ldt,
-                               int64_t r0, int64_t n, cudaStream_t st) {
+// n rows of w elements (host row stride ld) into a packed device tile. A
+// contiguous block goes as one linear copy: a 2-D copy of narrow rows (8-bit
+// A, small M) runs row by row far below the PCIe rate.
+template <class T>
+cudaError_t upload_rows(T* dst, const T* src, int64_t ld, int64_t w, int64_t n, cudaStream_t st) {
+  return ld == w ? cudaMemcpyAsync(dst, src, (size_t)n * w * sizeof(T), cudaMemcpyHostToDevice, st)
+                 : cudaMemcpy2DAsync(dst, w * sizeof(T), src, ld * sizeof(T), w * sizeof(T), n,
+                                     cudaMemcpyHostToDevice, st);
+}
+
+template <class T>
+cudaError_t download_rows(T* dst, int64_t ld, const T* src, int64_t w, int64_t n, cudaStream_t st) {
+  return ld == w ? cudaMemcpyAsync(dst, src, (size_t)n * w * sizeof(T), cudaMemcpyDeviceToHost, st)
+                 : cudaMemcpy2DAsync(dst, ld * sizeof(T), src, w * sizeof(T), w * sizeof(T), n,
+                                     cudaMemcpyDeviceToHost, st);
+}
+
+// Chunk [r0, r0 + n) of the split columns of host At (D x N, ldt) into the
+// slot's D x chunk column-major tile (ldt = chunk); rows of At that are not
+// split columns are never copied and never read. Adjacent columns as one 2-D
+// copy of n-float rows.
+cudaError_t upload_split_columns(const mdn_exec* x, float* dAt, const float* At, int64_t ldt,
+                                 int64_t r0, int64_t n, cudaStream_t st) {
   const std::vector<uint16_t>& cols = x->model->h_cols;
   cudaError_t e = cudaSuccess;
   for (size_t i = 0; i < cols.size() && e == cudaSuccess;) {
@@ -892,40 +798,54 @@ cudaError_t copy_split_columns(const mdn_exec* x, float* dAt, const float* At, i
   }
   return e;
 }
-}  // namespace
 
-// g on column-major host A: split columns in, packed codes out.
-int mdn_encode_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, uint8_t* codes) {
+// Fused g + f on host rows (fp32 or natively 8-bit).
+template <class TIn>
+int amm_host(mdn_exec* x, const TIn* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
   if (!x || N < 0) return MDN_EINVAL;
-  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_*_pq_host
+  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_amm_pq_host
   if (N == 0) return MDN_OK;
-  if (!At || !codes || ldt < N) return MDN_EINVAL;
-  DeviceGuard g(x->device);
-  if (!g.ok) return MDN_ECUDA;
-  const int64_t nb = (x->model->C + 1) / 2;
-  cudaError_t e = cudaSuccess;
-  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
-  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
-    const int s = (int)(q % x->n_slots);
-    cudaStream_t st = x->streams[s];
-    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
-    e = copy_split_columns(x, x->dA[s], At, ldt, r0, n, st);
-    if (e != cudaSuccess) break;
-    e = launch_encode_cm(x->model->trees(), x->dA[s], n, x->chunk, x->dC[s], st);
-    if (e != cudaSuccess) break;
-    e = cudaMemcpyAsync(codes + r0 * nb, x->dC[s], (size_t)n * nb, cudaMemcpyDeviceToHost, st);
-  }
-  for (auto s : x->streams) {
-    cudaError_t e2 = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) e = e2;
-  }
-  return cuda_status(e);
+  const int D = x->model->D, M = x->luts->M;
+  if (!A || !out || lda < D || ldo < M) return MDN_EINVAL;
+  return run_pipeline(x, N, [&](int s, cudaStream_t st, int64_t r0, int64_t n) {
+    TIn* dA = reinterpret_cast<TIn*>(x->dA[s]);        // sized for fp32 rows: 8-bit rows fit
+    cudaError_t e = upload_rows(dA, A + r0 * lda, lda, D, n, st);
+    if (e != cudaSuccess) return e;
+    if constexpr (sizeof(TIn) == 1)
+      e = launch_amm_u8(x->model->trees(), x->luts->dev(), dA, n, D, x->dOut[s], M, st);
+    else
+      e = launch_amm(x->model->trees(), x->luts->dev(), dA, n, D, x->dOut[s], M, st);
+    if (e != cudaSuccess) return e;
+    return download_rows(out + r0 * ldo, ldo, x->dOut[s], M, n, st);
+  });
 }
 
-// PQ comparator through host buffers: codes only (out == null)
-// or codes + scan + dequant per chunk on the device (the two-launch PQ amm).
-static int pq_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes,
-                   float* out, int64_t ldo) {
+// g alone on host rows (fp32 or 8-bit): packed codes back.
+template <class TIn>
+int encode_host(mdn_exec* x, const TIn* A, int64_t N, int64_t lda, uint8_t* codes) {
+  if (!x || N < 0) return MDN_EINVAL;
+  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_encode_pq_host
+  if (N == 0) return MDN_OK;
+  const int D = x->model->D;
+  const int64_t nb = (x->model->C + 1) / 2;
+  if (!A || !codes || lda < D) return MDN_EINVAL;
+  return run_pipeline(x, N, [&](int s, cudaStream_t st, int64_t r0, int64_t n) {
+    TIn* dA = reinterpret_cast<TIn*>(x->dA[s]);
+    cudaError_t e = upload_rows(dA, A + r0 * lda, lda, D, n, st);
+    if (e != cudaSuccess) return e;
+    if constexpr (sizeof(TIn) == 1)
+      e = launch_encode_u8(x->model->trees(), dA, n, D, x->dC[s], st);
+    else
+      e = launch_encode(x->model->trees(), dA, n, D, x->dC[s], st);
+    if (e != cudaSuccess) return e;
+    return download_rows(codes + r0 * nb, nb, x->dC[s], nb, n, st);
+  });
+}
+
+// The PQ comparator: codes only (out == null) or codes + scan +
+// dequant per chunk on the device (the two-launch PQ amm).
+int pq_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes, float* out,
+            int64_t ldo) {
   if (!x || N < 0) return MDN_EINVAL;
   const mdn_model* m = x->model;
   if (!m->pq) return MDN_ESTATE;
@@ -933,37 +853,53 @@ static int pq_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t*
   const int D = m->D, M = x->luts->M;
   const int64_t nb = (m->C + 1) / 2;
   if (!A || lda < D || (!codes && !out) || (out && ldo < M)) return MDN_EINVAL;
-  DeviceGuard g(x->device);
-  if (!g.ok) return MDN_ECUDA;
-  cudaError_t e = cudaSuccess;
-  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
-  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
-    const int s = (int)(q % x->n_slots);
-    cudaStream_t st = x->streams[s];
-    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
-    float* dA = x->dA[s];
-    e = lda == D ? cudaMemcpyAsync(dA, A + r0 * lda, (size_t)n * D * sizeof(float), cudaMemcpyHostToDevice, st)
-                 : cudaMemcpy2DAsync(dA, D * sizeof(float), A + r0 * lda, lda * sizeof(float),
-                                     D * sizeof(float), n, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) break;
-    e = launch_encode_pq(m->trees(), m->d_P, m->d_sub, m->d_sub_e, dA, n, D, x->dC[s], st);
-    if (e != cudaSuccess) break;
-    if (out) {
-      e = launch_scan(x->luts->dev(), x->dC[s], n, nullptr, x->dOut[s], M, st);
-      if (e != cudaSuccess) break;
-      e = ldo == M ? cudaMemcpyAsync(out + r0 * ldo, x->dOut[s], (size_t)n * M * sizeof(float),
-                                     cudaMemcpyDeviceToHost, st)
-                   : cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
-                                       M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
-    } else {
-      e = cudaMemcpyAsync(codes + r0 * nb, x->dC[s], (size_t)n * nb, cudaMemcpyDeviceToHost, st);
-    }
-  }
-  for (auto s : x->streams) {
-    cudaError_t e2 = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) e = e2;
-  }
-  return cuda_status(e);
+  return run_pipeline(x, N, [&](int s, cudaStream_t st, int64_t r0, int64_t n) {
+    cudaError_t e = upload_rows(x->dA[s], A + r0 * lda, lda, D, n, st);
+    if (e != cudaSuccess) return e;
+    e = launch_encode_pq(m->trees(), m->d_P, m->d_sub, m->d_sub_e, x->dA[s], n, D, x->dC[s], st);
+    if (e != cudaSuccess) return e;
+    if (!out) return download_rows(codes + r0 * nb, nb, x->dC[s], nb, n, st);
+    e = launch_scan(x->luts->dev(), x->dC[s], n, nullptr, x->dOut[s], M, st);
+    if (e != cudaSuccess) return e;
+    return download_rows(out + r0 * ldo, ldo, x->dOut[s], M, n, st);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int mdn_amm_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* out, int64_t ldo) {
+  return amm_host<float>(x, A, N, lda, out, ldo);
+}
+
+int mdn_amm_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, float* out,
+                    int64_t ldo) {
+  return amm_host<uint8_t>(x, A, N, lda, out, ldo);
+}
+
+int mdn_encode_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes) {
+  return encode_host<float>(x, A, N, lda, codes);
+}
+
+int mdn_encode_host_u8(mdn_exec* x, const uint8_t* A, int64_t N, int64_t lda, uint8_t* codes) {
+  return encode_host<uint8_t>(x, A, N, lda, codes);
+}
+
+// f alone: host codes in, dequantised host rows out, with the executor's tables.
+int mdn_scan_host(mdn_exec* x, const uint8_t* codes, int64_t N, float* out, int64_t ldo) {
+  if (!x || N < 0) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  const int M = x->luts->M;
+  const int64_t nb = (x->model->C + 1) / 2;
+  if (!codes || !out || ldo < M) return MDN_EINVAL;
+  return run_pipeline(x, N, [&](int s, cudaStream_t st, int64_t r0, int64_t n) {
+    cudaError_t e = upload_rows(x->dC[s], codes + r0 * nb, nb, nb, n, st);
+    if (e != cudaSuccess) return e;
+    e = launch_scan(x->luts->dev(), x->dC[s], n, nullptr, x->dOut[s], M, st);
+    if (e != cudaSuccess) return e;
+    return download_rows(out + r0 * ldo, ldo, x->dOut[s], M, n, st);
+  });
 }
 
 int mdn_encode_pq_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, uint8_t* codes) {
@@ -976,41 +912,37 @@ int mdn_amm_pq_host(mdn_exec* x, const float* A, int64_t N, int64_t lda, float* 
   return pq_host(x, A, N, lda, nullptr, out, ldo);
 }
 
-// Column-major host A: per chunk only the distinct split columns
-// cross PCIe (4 |S| instead of 4 D bytes per row). The slot buffer is used as
-// a D x chunk column-major tile (ldt = chunk); rows of At that are not split
-// columns are never copied and never read. Consecutive split columns go as
-// one 2-D copy (rows of n floats, pitches ldt and chunk).
+// Column-major host A: only the split columns cross PCIe
+// (4 |S| instead of 4 D bytes per row).
 int mdn_amm_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, float* out,
                     int64_t ldo) {
   if (!x || N < 0) return MDN_EINVAL;
-  if (x->model->pq) return MDN_ESTATE;                 // PQ model: mdn_*_pq_host
+  if (x->model->pq) return MDN_ESTATE;
   if (N == 0) return MDN_OK;
   const int M = x->luts->M;
   if (!At || !out || ldt < N || ldo < M) return MDN_EINVAL;
-  DeviceGuard g(x->device);
-  if (!g.ok) return MDN_ECUDA;
-  cudaError_t e = cudaSuccess;
-  const int64_t nchunks = (N + x->chunk - 1) / x->chunk;
-  for (int64_t q = 0; q < nchunks && e == cudaSuccess; ++q) {
-    const int s = (int)(q % x->n_slots);
-    cudaStream_t st = x->streams[s];
-    const int64_t r0 = q * x->chunk, n = N - r0 < x->chunk ? N - r0 : x->chunk;
-    float* dAt = x->dA[s];
-    e = copy_split_columns(x, dAt, At, ldt, r0, n, st);
-    if (e != cudaSuccess) break;
-    e = launch_amm_cm(x->model->trees(), x->luts->dev(), dAt, n, x->chunk, x->dOut[s], M, st);
-    if (e != cudaSuccess) break;
-    e = ldo == M ? cudaMemcpyAsync(out + r0 * ldo, x->dOut[s], (size_t)n * M * sizeof(float),
-                                   cudaMemcpyDeviceToHost, st)
-                 : cudaMemcpy2DAsync(out + r0 * ldo, ldo * sizeof(float), x->dOut[s], M * sizeof(float),
-                                     M * sizeof(float), n, cudaMemcpyDeviceToHost, st);
-  }
-  for (auto s : x->streams) {
-    cudaError_t e2 = cudaStreamSynchronize(s);
-    if (e == cudaSuccess) e = e2;
-  }
-  return cuda_status(e);
+  return run_pipeline(x, N, [&](int s, cudaStream_t st, int64_t r0, int64_t n) {
+    cudaError_t e = upload_split_columns(x, x->dA[s], At, ldt, r0, n, st);
+    if (e != cudaSuccess) return e;
+    e = launch_amm_cm(x->model->trees(), x->luts->dev(), x->dA[s], n, x->chunk, x->dOut[s], M, st);
+    if (e != cudaSuccess) return e;
+    return download_rows(out + r0 * ldo, ldo, x->dOut[s], M, n, st);
+  });
+}
+
+int mdn_encode_cm_host(mdn_exec* x, const float* At, int64_t N, int64_t ldt, uint8_t* codes) {
+  if (!x || N < 0) return MDN_EINVAL;
+  if (x->model->pq) return MDN_ESTATE;
+  if (N == 0) return MDN_OK;
+  if (!At || !codes || ldt < N) return MDN_EINVAL;
+  const int64_t nb = (x->model->C + 1) / 2;
+  return run_pipeline(x, N, [&](int s, cudaStream_t st, int64_t r0, int64_t n) {
+    cudaError_t e = upload_split_columns(x, x->dA[s], At, ldt, r0, n, st);
+    if (e != cudaSuccess) return e;
+    e = launch_encode_cm(x->model->trees(), x->dA[s], n, x->chunk, x->dC[s], st);
+    if (e != cudaSuccess) return e;
+    return download_rows(codes + r0 * nb, nb, x->dC[s], nb, n, st);
+  });
 }
 
 }  // extern "C"
