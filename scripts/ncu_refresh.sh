@@ -12,6 +12,9 @@ bash scripts/ncu_capture.sh \
   image_u8_exact k_amm_rt --config image_u8 -- \
   cls100_col_exact k_amm_ws --config cls100 --layout col -- \
   scale_col_exact k_amm_ws --config scale --layout col -- \
+  tiny_col_exact k_amm_cm --config tiny --layout col -- \
+  image_col_exact k_amm_cm --config image --layout col -- \
+  tiny_col_encode_exact k_amm_cm --config tiny --layout col --op encode -- \
   cls100_col_encode_exact k_amm_ws --config cls100 --layout col --op encode -- \
   cls100_encode_exact k_amm_ws --config cls100 --op encode -- \
   image_encode_exact k_amm_rt --config image --op encode -- \
