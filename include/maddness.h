@@ -202,11 +202,19 @@ int mdn_encode_pq(const mdn_model* model, const float* A, int64_t N, int64_t lda
 /* ----------------------------------------------------- end-to-end (host) -- */
 
 /* A pipelined executor for HOST buffers: row chunks are copied host->device,
- * run through the fused kernel and copied back, with the copies of one chunk
+ * run through the device op and copied back, with the copies of one chunk
  * overlapping the kernel of another (`n_slots` device staging slots of
- * `chunk_rows` rows, one stream each). Owns its device staging buffers and
+ * `chunk_rows` rows, one stream each; chunk q uses slot q % n_slots and stream
+ * order serialises a slot's reuse). Owns its device staging buffers and
  * streams; `model` and `luts` are borrowed and must outlive the executor.
- * For overlap the host buffers should be page-locked. */
+ * For overlap the host buffers should be page-locked. Every host call below
+ * is synchronous (returns when the host outputs hold every row); N = 0 is a
+ * no-op; null buffers or short strides -> MDN_EINVAL; a call for the other
+ * model kind (tree calls on a PQ executor, PQ calls on a MADDNESS one) ->
+ * MDN_ESTATE; CUDA failures -> MDN_ECUDA.
+ * Errors: luts from another model -> MDN_ESTATE, C mismatch -> MDN_ESHAPE,
+ * chunk_rows < 1 or n_slots outside [1, 8] -> MDN_EINVAL, allocation ->
+ * MDN_ENOMEM. */
 int mdn_exec_create(const mdn_model* model, const mdn_luts* luts, int64_t chunk_rows,
                     int n_slots, mdn_exec** out);
 void mdn_exec_free(mdn_exec* exec);
