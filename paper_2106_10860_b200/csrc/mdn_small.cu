@@ -117,6 +117,8 @@ __device__ __forceinline__ uint32_t tree_code(V x0, V x1, V x2, V x3, const V (&
 //   is the compare.
 struct ByteTree {
   int q0, q2, d12;                 // level 0 threshold; level 1: v = q2 + lt0 * (q1 - q2)
+  uint32_t s01;                    // PRMT selector: x1 in bits 0-7, x0 in bits 16-23
+  uint32_t q0s, nq2s, nd12s;       // q0 << 16, -(q2 << 16), -((q1 - q2) << 16)
   uint32_t Q2, Q3lo, Q3hi;         // level tables, byte n = threshold of complemented node n
   uint32_t s0, s1, s2, s3;         // PRMT selectors of the split values in the subspace word
   uint32_t g2, g3;                 // byte 0 of Q2 / Q3lo (pad bytes of the packed compares)
@@ -144,11 +146,32 @@ __device__ __forceinline__ uint32_t push_sign(uint32_t n, uint32_t d) {
   return r;
 }
 
+#ifndef MDN_BQ01
+#define MDN_BQ01 1   // levels 0 and 1 from one PRMT (x1 + (x0 << 16)); 0: one PRMT each
+#endif
+static __constant__ uint32_t k_shift16 = 65536u;   // opaque to ptxas: the multiply stays an IMAD
+
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 // 15 - code (the complemented leaf index n_4) for 8-bit rows; see byte_tree_addr.
+// Levels 0 and 1 (MDN_BQ01): r = x1 + (x0 << 16) from one PRMT; r - (q0 << 16)
+// is negative iff x0 < q0 (x1 < 2^16 cannot carry into the sign), and
+// r * 2^16 - (v1 << 16) = (x1 - v1) << 16 has the sign of x1 - v1 (|x1 - v1|
+// < 2^8), both products on the FMA pipe.
 __device__ __forceinline__ uint32_t byte_tree_n4(uint32_t w, const ByteTree& b) {
+#if MDN_BQ01
+  const uint32_t r = prmt(w, 0u, b.s01);
+  const uint32_t lt0 = sign_bit(r - b.q0s);
+  const uint32_t n2 = push_sign(lt0, mad_lo(r, k_shift16, mad_lo(lt0, b.nd12s, b.nq2s)));
+#else
   const uint32_t lt0 = sign_bit(prmt(w, 0u, b.s0) - (uint32_t)b.q0);
   const uint32_t v1 = (uint32_t)b.q2 + lt0 * (uint32_t)b.d12;
   const uint32_t n2 = push_sign(lt0, prmt(w, 0u, b.s1) - v1);
+#endif
   const uint32_t n3 = push_sign(n2, prmt(w, b.g2, b.s2) - prmt(b.Q2, b.Q2, n2));
   return push_sign(n3, prmt(w, b.g3, b.s3) - prmt(b.Q3lo, b.Q3hi, n3));
 }
@@ -280,6 +303,10 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
     const uint32_t j0 = o[0] - sub, j1 = o[1] - sub, j2 = o[2] - sub, j3 = o[3] - sub;
     bt.s0 = j0 | 0x4440u;
     bt.s1 = j1 | 0x4440u;
+    bt.s01 = j1 | 0x40u | (j0 << 8) | 0x4000u;    // (x1, 0, x0, 0)
+    bt.q0s = (uint32_t)bt.q0 << 16;
+    bt.nq2s = 0u - ((uint32_t)bt.q2 << 16);
+    bt.nd12s = 0u - ((uint32_t)bt.d12 << 16);
     bt.s2 = j2 | 0x4440u;                          // (x, g, g, g)
     bt.s3 = j3 | 0x4440u;
     bt.base = lut_c + 15u * 4u * W2;
