@@ -51,10 +51,21 @@ namespace fast {
 namespace small {
 
 constexpr int R = 256;                   // rows per stage (= TMA box rows)
-constexpr int CPS = R / 32;              // 32-row chunks per stage = warps per group
-constexpr int NG = 2;                    // worker groups
-constexpr int NWK = NG * CPS;            // worker warps
+constexpr int NWK = 16;                  // worker warps
 constexpr int THREADS = 32 * (1 + NWK);
+#ifndef MDN_RT_SUBS_U8_ENC
+#define MDN_RT_SUBS_U8_ENC 2 // 32-row chunks an 8-bit encode-only worker takes per stage
+#endif
+// A worker takes SUBS consecutive 32-row chunks of a stage (one barrier wait
+// and release per SUBS chunks); CPS workers share a stage, NG groups rotate.
+// Two chunks per wait pay only where the per-stage overhead is a visible share
+// of the work: the 8-bit encode-only kernel (same box: 1.285 -> 1.389e11
+// rows/s); the fused 8-bit kernel lost 2.4% with it, fp32 rows are HBM-bound.
+template <class TIn, bool ENC> constexpr int subs_of() {
+  return sizeof(TIn) == 1 && ENC ? MDN_RT_SUBS_U8_ENC : 1;
+}
+template <class TIn, bool ENC> constexpr int cps_of() { return R / (32 * subs_of<TIn, ENC>()); }
+template <class TIn, bool ENC> constexpr int ng_of() { return NWK / cps_of<TIn, ENC>(); }
 constexpr int NS_MAX = 8;
 #ifndef MDN_RT_CTAS_U8
 #define MDN_RT_CTAS_U8 1     // resident CTAs per SM of the 8-bit variants (tuning: -DMDN_RT_CTAS_U8=2)
@@ -214,6 +225,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
   // and the stage holds a third fewer bytes.
   constexpr int PITCH = sizeof(TIn) == 1 ? D : D + 16 / (int)sizeof(TIn);
   constexpr int RPW = 32 / C;                       // rows per encode iteration
+  constexpr int SUBS = subs_of<TIn, ENC>(), CPS = cps_of<TIn, ENC>(), NG = ng_of<TIn, ENC>();
   constexpr int CS = CodeStride<C>::value;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -326,14 +338,16 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
   int s = grp, ph = 0;
   while (s >= p.NS) s -= p.NS, ph ^= 1;
   // This lane's output row and pointer, advanced by a constant stride per stage.
-  int64_t row = ((int64_t)blockIdx.x + (int64_t)grp * gridDim.x) * R + chunk * 32 + lane;
+  int64_t row = ((int64_t)blockIdx.x + (int64_t)grp * gridDim.x) * R + chunk * 32 * SUBS + lane;
   const int64_t row_step = (int64_t)NG * gridDim.x * R;
   float* o_row = p.out + row * p.ldo;
   const int64_t o_step = row_step * p.ldo;
   for (int64_t q = grp; q < n_local; q += NG, row += row_step, o_row += o_step) {
     mbar_wait_sleep(&full[s], (uint32_t)ph);
+#pragma unroll 1
+    for (int hs = 0; hs < SUBS; ++hs) {
     const TIn* stg = reinterpret_cast<const TIn*>(smem + OFF_STAGE + (size_t)s * p.stage_b) +
-                     (size_t)(chunk * 32 + rs) * PITCH;
+                     (size_t)(chunk * 32 * SUBS + hs * 32 + rs) * PITCH;
     // ---- encode 32 rows: C iterations of RPW rows x C codebooks ----
     // All loads first, then the (independent) trees, then the stores, so the
     // compiler may interleave the C dependency chains.
@@ -380,7 +394,8 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
         const uint32_t r = __shfl_xor_sync(0xffffffffu, t, 1 << k);
         keep = (keep & t_sel[k]) | (r & ~t_sel[k]);
       }
-      const int64_t r = ((int64_t)blockIdx.x + q * gridDim.x) * R + chunk * 32 + c * RPW + rs;
+      const int64_t r = ((int64_t)blockIdx.x + q * gridDim.x) * R + chunk * 32 * SUBS + hs * 32 +
+                        c * RPW + rs;
       if (r < p.N) {
         if constexpr (C == 8)
           reinterpret_cast<uint32_t*>(p.codes)[r] = keep;
@@ -388,10 +403,8 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
           reinterpret_cast<uint16_t*>(p.codes)[r] = (uint16_t)keep;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      s += NG;
-      while (s >= p.NS) s -= p.NS, ph ^= 1;
-      continue;
+      if (hs == SUBS - 1 && lane == 0) mbar_arrive(&empty[s]);
+      continue;                                      // next chunk of this stage
     }
 #pragma unroll
     for (int it = 0; it < C; ++it) {
@@ -399,7 +412,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
       s_code[rr * CS + (C == 8 ? (c ^ (rr & 4)) : c)] = code[it];
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);           // this chunk's rows are consumed
+    if (hs == SUBS - 1 && lane == 0) mbar_arrive(&empty[s]);   // the stage's rows are consumed
     // ---- scan row `lane` ----
     uint32_t off[C];
 #pragma unroll
@@ -436,7 +449,8 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
           acc[w] += v[0];
         }
     }
-    if (row < p.N) {
+    if (row + hs * 32 < p.N) {
+      float* o_h = o_row + (int64_t)hs * 32 * p.ldo;
       float f[2 * W2];
 #pragma unroll
       for (int w = 0; w < W2; ++w) {
@@ -447,18 +461,19 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
         if constexpr (W2 % 2 == 0) {
 #pragma unroll
           for (int w = 0; w < W2; w += 2)
-            *reinterpret_cast<float4*>(o_row + 2 * w) = make_float4(f[2 * w], f[2 * w + 1], f[2 * w + 2], f[2 * w + 3]);
+            *reinterpret_cast<float4*>(o_h + 2 * w) = make_float4(f[2 * w], f[2 * w + 1], f[2 * w + 2], f[2 * w + 3]);
         } else {
 #pragma unroll
           for (int w = 0; w < W2; ++w)
-            *reinterpret_cast<float2*>(o_row + 2 * w) = make_float2(f[2 * w], f[2 * w + 1]);
+            *reinterpret_cast<float2*>(o_h + 2 * w) = make_float2(f[2 * w], f[2 * w + 1]);
         }
       } else {
 #pragma unroll
         for (int m = 0; m < 2 * W2; ++m)
-          if (m < p.M) o_row[m] = f[m];
+          if (m < p.M) o_h[m] = f[m];
       }
     }
+    }  // chunks of the stage
     s += NG;
     while (s >= p.NS) s -= p.NS, ph ^= 1;
   }
@@ -528,6 +543,7 @@ static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int
   const size_t fixed = ((256 + (size_t)t.C * 16 * W2 * 4 + (size_t)NWK * 32 * (t.C == 8 ? 12 : 4) * 4) + 127) & ~size_t(127);
   size_t budget = (size_t)dev_info().smem_optin;
   if (es == 1 && MDN_RT_CTAS_U8 > 1) budget = std::min(budget, (size_t)(233472 / MDN_RT_CTAS_U8 - 1024));
+  constexpr int NG = ng_of<TIn, false>();
   if (fixed + (size_t)2 * NG * stage_b > budget) return cudaSuccess;
   int NS = (int)((budget - fixed) / stage_b);
   if (NS > NS_MAX) NS = NS_MAX;
@@ -585,6 +601,7 @@ static cudaError_t encode_rt(const TreesDev& t, const TIn* A, int64_t N, int64_t
   const size_t fixed = 256;                          // barriers only (kernel's OFF_STAGE)
   size_t budget = (size_t)dev_info().smem_optin;
   if (es == 1 && MDN_RT_CTAS_U8 > 1) budget = std::min(budget, (size_t)(233472 / MDN_RT_CTAS_U8 - 1024));
+  constexpr int NG = ng_of<TIn, true>();
   int NS = (int)((budget - fixed) / stage_b);
   if (NS > NS_MAX) NS = NS_MAX;
   NS -= NS % NG;
