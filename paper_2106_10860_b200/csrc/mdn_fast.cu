@@ -68,6 +68,9 @@ __host__ __device__ constexpr int off_base(int c) { return 4 * c + 4 * (c >> 3);
 #define MDN_CM_MIX 3
 #endif
 
+#ifndef MDN_E_WIDE
+#define MDN_E_WIDE 2         // encoder warps of the row-major kernel for W >= 8 (cls100)
+#endif
 #ifndef MDN_CM_E
 #define MDN_CM_E 6           // encoder warps of the column-major kernel for W >= 8 (cls100)
 #endif
@@ -80,7 +83,7 @@ struct Roles {
   // Column-major A with wide tables runs ~35% more rows/s than row-major
   // (fewer bytes per row), so it gets 6 encoder warps instead of 2 (cls100:
   // 3.65 -> 4.11e9 rows/s; 2 encoder warps could not keep up).
-  static constexpr int E = ENC_ONLY ? 8 : (W >= 8 ? (CMV ? MDN_CM_E : 2) : (W >= 3 ? MDN_E_MID : 8));
+  static constexpr int E = ENC_ONLY ? 8 : (W >= 8 ? (CMV ? MDN_CM_E : MDN_E_WIDE) : (W >= 3 ? MDN_E_MID : 8));
   static constexpr int S = ENC_ONLY ? 0 : (W >= 8 ? 8 : (W >= 3 ? 4 : 2));
   static constexpr int THREADS = 32 * (1 + E + S);
   static constexpr int ROWS_PER_SCANNER = ENC_ONLY ? 0 : BR / (32 * S);
