@@ -165,6 +165,13 @@ def test_null_handle_guards_every_hot_path_call(lib):
         "mdn_scan": ([P, P, I, P, P, I, P], (None, None, 1, None, None, 1, None)),
         "mdn_amm_host": ([P, P, I, I, P, I], (None, None, 1, 1, None, 1)),
         "mdn_amm_host_u8": ([P, P, I, I, P, I], (None, None, 1, 1, None, 1)),
+        "mdn_encode_host": ([P, P, I, I, P], (None, None, 1, 1, None)),
+        "mdn_encode_host_u8": ([P, P, I, I, P], (None, None, 1, 1, None)),
+        "mdn_scan_host": ([P, P, I, P, I], (None, None, 1, None, 1)),
+        "mdn_amm_cm_host": ([P, P, I, I, P, I], (None, None, 1, 1, None, 1)),
+        "mdn_encode_cm_host": ([P, P, I, I, P], (None, None, 1, 1, None)),
+        "mdn_encode_pq_host": ([P, P, I, I, P], (None, None, 1, 1, None)),
+        "mdn_amm_pq_host": ([P, P, I, I, P, I], (None, None, 1, 1, None, 1)),
     }
     for name, (argtypes, args) in calls.items():
         f = getattr(lib, name)
@@ -173,3 +180,22 @@ def test_null_handle_guards_every_hot_path_call(lib):
     # negative N is rejected too
     lib.mdn_encode.argtypes = [P, P, I, I, P, P]
     assert lib.mdn_encode(None, None, -1, 1, None, None) == -1
+
+
+def test_package_without_library_fails_loudly(tmp_path):
+    """The product path has no CPU fallback: importing the binding from a copy
+    of the package that lacks libmaddness.so raises ImportError."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = os.path.join(ROOT, "paper_2106_10860_b200")
+    dst = tmp_path / "paper_2106_10860_b200"
+    dst.mkdir()
+    for name in os.listdir(pkg):
+        if name.endswith(".py"):
+            shutil.copy(os.path.join(pkg, name), dst / name)
+    r = subprocess.run([sys.executable, "-c", "import paper_2106_10860_b200"], cwd=tmp_path,
+                       env=dict(os.environ, PYTHONPATH=str(tmp_path)), capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode != 0
+    assert "ImportError" in r.stderr and "no CPU fallback" in r.stderr
