@@ -31,8 +31,11 @@
  *    current device before returning. `stream` is a cudaStream_t (NULL = the
  *    legacy default stream); all work of a call is enqueued on it.
  *  - Layouts are row-major with explicit leading dimensions in elements.
- *  - Handles are immutable after creation and may be used concurrently from
- *    several host threads / streams.
+ *  - Model and LUT handles are immutable after creation and may be used
+ *    concurrently from several host threads / streams. An executor
+ *    (mdn_exec) owns mutable staging slots: concurrent host calls on ONE
+ *    executor are serialised by its internal lock (safe, not parallel); use
+ *    one executor per thread for parallel host pipelines.
  *  - N = 0 is a no-op returning MDN_OK.
  */
 #ifndef MADDNESS_H_
@@ -89,7 +92,8 @@ int mdn_model_info(const mdn_model* model, int* C, int* D, uint64_t* fingerprint
  * Algorithms 3/4 (L252-305, L621-682), then ridge prototypes
  * P = (G^T G + lambda I)^-1 G^T A~ (L318-321), or bucket means for lambda = 0
  * (L218) -- with the readings R1-R12 of DESIGN.md.
- *   A       device fp32 training rows A~, N x D, row stride lda >= D.
+ *   A       device fp32 training rows A~, N x D, row stride lda >= D;
+ *           1 <= N <= 2^31 - 2^20 - 1 (int32 row indices with loop headroom).
  *   buf     host buffer receiving a "model.mdnm v1" stream (load it with
  *           mdn_model_load); buf == NULL: *len receives the size needed,
  *           48 + 76 C + 64 C D + 8 bytes. Otherwise *len is the capacity in,
@@ -104,7 +108,8 @@ int mdn_train(const float* A, int64_t N, int64_t lda, int D, int C, double lambd
 /* h(B) + App. A quantisation (the "set_operator" step), computed on the device.
  *   B     HOST fp32, D x M row-major, row stride ldb >= M (elements).
  *   mode  MDN_SUM_EXACT or MDN_SUM_AVG.
- *   U     averaging block (power of two dividing C); ignored in exact mode.
+ *   U     averaging block (power of two dividing C, U <= 64); ignored in
+ *         exact mode (stored as 1).
  * Arithmetic (reading R13-R15, R18 of DESIGN.md):
  *   T[c][k][m] = sum_{j ascending} (double)P[16c+k][j] * (double)B[j][m]
  *   delta_c = min_{k,m} T[c];  R = max_c max_{k,m}(T[c] - delta_c)
@@ -118,7 +123,11 @@ int mdn_build_luts(const mdn_model* model, const float* B, int64_t M, int64_t ld
 /* Serialize to "luts.mdnl v1". buf == NULL: *len receives the size needed.
  * Otherwise *len is the capacity in, bytes written out (MDN_EINVAL if small). */
 int mdn_luts_serialize(const mdn_luts* luts, void* buf, size_t* len);
-/* Load a "luts.mdnl v1" stream (e.g. after an NCCL broadcast) onto `device`. */
+/* Load a "luts.mdnl v1" stream (e.g. after an NCCL broadcast) onto `device`.
+ * Validates what mdn_build_luts enforces: bad magic / truncation / checksum
+ * -> MDN_EFORMAT (*err_off = offending byte), version != 1 -> MDN_EVERSION,
+ * C outside [1, 256], M outside [1, 4096], unknown mode, U not a power of
+ * two dividing C, U > 64, or U != 1 in exact mode -> MDN_EINVAL. */
 int mdn_luts_load(const void* buf, size_t len, int device, mdn_luts** out,
                   size_t* err_off);
 void mdn_luts_free(mdn_luts* luts);
@@ -213,8 +222,9 @@ int mdn_encode_pq(const mdn_model* model, const float* A, int64_t N, int64_t lda
  * model kind (tree calls on a PQ executor, PQ calls on a MADDNESS one) ->
  * MDN_ESTATE; CUDA failures -> MDN_ECUDA.
  * Errors: luts from another model -> MDN_ESTATE, C mismatch -> MDN_ESHAPE,
- * chunk_rows < 1 or n_slots outside [1, 8] -> MDN_EINVAL, allocation ->
- * MDN_ENOMEM. */
+ * chunk_rows < 1 or n_slots outside [1, 8], or luts on another device than
+ * the model -> MDN_EINVAL, allocation -> MDN_ENOMEM. Host calls on one
+ * executor from several threads run one after another (internal lock). */
 int mdn_exec_create(const mdn_model* model, const mdn_luts* luts, int64_t chunk_rows,
                     int n_slots, mdn_exec** out);
 void mdn_exec_free(mdn_exec* exec);

@@ -229,7 +229,7 @@ __global__ void k_amm_cm_generic(TreesDev t, LutsDev l, const float* __restrict_
       } else {
         // App. D halves recursion, evaluated as a binary counter (as mdn_generic.cu)
         for (int b = 0; b < l.C / l.U; ++b) {
-          int stack[8], top = 0;
+          int stack[AVG_STACK], top = 0;
           for (int i = 0; i < l.U; ++i) {
             const int c = b * l.U + i;
             int v = l.tq[((int64_t)c * K + ((code_row[c >> 1] >> (4 * (c & 1))) & 15)) * l.M + m];

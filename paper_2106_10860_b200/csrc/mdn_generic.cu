@@ -88,7 +88,7 @@ __device__ __forceinline__ int sum_entry(const uint8_t* __restrict__ tq, const u
   }
   int total = 0;
   for (int b = 0; b < C / U; ++b) {
-    int stack[8];
+    int stack[AVG_STACK];
     int top = 0;
     for (int i = 0; i < U; ++i) {
       int c = b * U + i;

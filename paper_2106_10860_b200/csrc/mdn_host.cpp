@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -312,7 +313,7 @@ int mdn_train(const float* A, int64_t N, int64_t lda, int D, int C, double lambd
     *len = need;
     return MDN_OK;
   }
-  if (*len < need || !A || N < 1 || N > 0x7FFFFFFF || lda < D) return MDN_EINVAL;
+  if (*len < need || !A || N < 1 || N > MDN_TRAIN_MAX_N || lda < D) return MDN_EINVAL;
   DeviceGuard g(device);
   if (!g.ok) return MDN_ECUDA;
   std::vector<uint8_t> blob;
@@ -373,7 +374,7 @@ int mdn_build_luts(const mdn_model* m, const float* B, int64_t M, int64_t ldb, i
                    mdn_luts** out) {
   if (!m || !B || !out || M < 1 || M > 4096 || ldb < M) return MDN_EINVAL;
   if (mode != MDN_SUM_EXACT && mode != MDN_SUM_AVG) return MDN_EINVAL;
-  if (mode == MDN_SUM_AVG && (!is_pow2(U) || m->C % U != 0 || U > 64)) return MDN_EINVAL;
+  if (mode == MDN_SUM_AVG && (!is_pow2(U) || m->C % U != 0 || U > MAX_U)) return MDN_EINVAL;
   if (mode == MDN_SUM_EXACT) U = 1;
   *out = nullptr;
   DeviceGuard g(m->device);
@@ -479,8 +480,9 @@ int mdn_luts_load(const void* buf, size_t len, int device, mdn_luts** out, size_
   uint32_t k = r.get<uint32_t>(), mode = r.get<uint32_t>(), U = r.get<uint32_t>();
   if (ver != 1) return set_err(err_off, 4, MDN_EVERSION);
   if (k != (uint32_t)K || C < 1 || C > (uint32_t)MAX_C || M < 1 || M > 4096 || mode > 1 ||
-      !is_pow2((int)U) || C % U != 0)
-    return set_err(err_off, 8, MDN_EINVAL);
+      !is_pow2((int)U) || C % U != 0 || U > (uint32_t)MAX_U ||
+      (mode == MDN_SUM_EXACT && U != 1))
+    return set_err(err_off, 8, MDN_EINVAL);   // same U rule as mdn_build_luts
   int32_t lexp = r.get<int32_t>();
   float alpha = r.get<float>(), beta = r.get<float>();
   uint64_t mfp = r.get<uint64_t>();
@@ -680,6 +682,7 @@ struct mdn_exec {
   std::vector<cudaStream_t> streams;
   std::vector<float*> dA, dOut;
   std::vector<uint8_t*> dC;       // packed codes of a chunk (mdn_encode_host / mdn_scan_host)
+  std::mutex mu;                  // held for a whole host call: the slots are per handle
 };
 
 void mdn_exec_free(mdn_exec* x) {
@@ -699,6 +702,7 @@ int mdn_exec_create(const mdn_model* m, const mdn_luts* l, int64_t chunk_rows, i
   if (!m || !l || !out || chunk_rows < 1 || n_slots < 1 || n_slots > 8) return MDN_EINVAL;
   if (l->C != m->C) return MDN_ESHAPE;
   if (l->model_fp != m->fingerprint) return MDN_ESTATE;
+  if (l->device != m->device) return MDN_EINVAL;   // as mdn_amm: tables on the model's device
   *out = nullptr;
   DeviceGuard g(m->device);
   if (!g.ok) return MDN_ECUDA;
@@ -746,6 +750,9 @@ namespace {
 
 template <class ChunkFn>
 int run_pipeline(mdn_exec* x, int64_t N, ChunkFn&& chunk) {
+  // The staging slots are mutable state of the handle: one call at a time
+  // (maddness.h: concurrent calls on one executor serialise here).
+  std::lock_guard<std::mutex> lock(x->mu);
   DeviceGuard g(x->device);
   if (!g.ok) return MDN_ECUDA;
   cudaError_t e = cudaSuccess;

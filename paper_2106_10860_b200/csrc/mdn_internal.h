@@ -15,6 +15,12 @@ namespace mdn {
 constexpr int K = MDN_K;           // leaves per tree
 constexpr int THR_STRIDE = 16;     // 15 heap-ordered thresholds + 1 pad per codebook
 constexpr int MAX_C = 256;         // S <= 255 * C must fit the 16-bit SWAR lanes
+// Training rows are int32 indices; the block-stride loops (i += blockDim <= 1024)
+// need headroom below INT32_MAX so that i + stride never overflows.
+constexpr int64_t MDN_TRAIN_MAX_N = 0x7FFFFFFF - (1 << 20);
+constexpr int MAX_U = 64;          // largest averaging block (App. D; U = 16 default)
+constexpr int AVG_STACK = 7;       // log2(MAX_U) + 1 levels of the halves-recursion stack
+static_assert((1 << (AVG_STACK - 1)) == MAX_U, "averaging stack depth must match MAX_U");
 constexpr int MAX_W2 = 4;          // words16 tables are kept for M <= 8
 
 // Tree parameters as the kernels consume them (device).

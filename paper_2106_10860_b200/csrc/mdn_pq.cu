@@ -152,7 +152,8 @@ cudaError_t launch_encode_pq(const TreesDev& t, const float* P_dense, const uint
                              const uint16_t* sub_e, const float* A, int64_t N, int64_t lda,
                              uint8_t* codes, cudaStream_t s) {
   const bool fast_ok = t.pq_cent && t.pq_ds > 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
-                       lda % 4 == 0 && t.C % 2 == 0;
+                       lda % 4 == 0 && t.C % 2 == 0 &&
+                       (size_t)16 * t.pq_ds * t.C * 4 <= (size_t)fast::dev_info().smem_optin;
   if (fast_ok) {
     switch (t.pq_ds) {
       case 4: return launch<4, 8>(A, N, lda, t.C, t.pq_cent, codes, s);

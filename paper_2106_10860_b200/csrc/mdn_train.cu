@@ -94,7 +94,8 @@ __global__ void k_gather_keys(const float* __restrict__ A, int64_t lda, const in
   const int c = blockIdx.y;
   const int col = cols[c];
   const size_t off = (size_t)c * N;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
     const int r = perm[off + i];
     keys[off + i] = A[(int64_t)r * lda + col] + 0.0f;
     vals[off + i] = r;

@@ -91,6 +91,14 @@ def test_luts_parser_errors(lib):
     assert lib.mdn_luts_load(hdr, len(hdr), 0, ct.byref(h), ct.byref(off)) == -4
     hdr = b"MDNL" + struct.pack("<6I", 1, 4, 4, 16, 1, 3) + b"\0" * 40   # U not pow2
     assert lib.mdn_luts_load(hdr, len(hdr), 0, ct.byref(h), ct.byref(off)) == -1
+    # U above the averaging-stack bound (mdn_build_luts caps U at 64): a crafted
+    # blob must not reach the generic kernels' fixed-depth halves-recursion stack
+    hdr = b"MDNL" + struct.pack("<6I", 1, 256, 4, 16, 1, 256) + b"\0" * 40
+    assert lib.mdn_luts_load(hdr, len(hdr), 0, ct.byref(h), ct.byref(off)) == -1
+    hdr = b"MDNL" + struct.pack("<6I", 1, 128, 4, 16, 1, 128) + b"\0" * 40
+    assert lib.mdn_luts_load(hdr, len(hdr), 0, ct.byref(h), ct.byref(off)) == -1
+    hdr = b"MDNL" + struct.pack("<6I", 1, 8, 4, 16, 0, 2) + b"\0" * 40    # exact mode, U != 1
+    assert lib.mdn_luts_load(hdr, len(hdr), 0, ct.byref(h), ct.byref(off)) == -1
 
 
 def test_null_and_shape_guards(lib):
