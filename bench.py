@@ -96,6 +96,53 @@ def _clock_summary(proc, t0=None, t1=None):
 
 
 ORACLE_CHUNK = 16384
+PARITY_ROWS = 4096
+
+
+def csrc_sha256() -> str:
+    """Hash of the library sources: ties a committed ncu traffic figure to
+    the kernel code it was measured on (profiles/traffic.json `_meta`)."""
+    import hashlib
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2106_10860_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        h.update(f.encode())
+        h.update(open(os.path.join(d, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def traffic_lookup(key: str):
+    """ncu DRAM bytes per launch of this line's kernel from the committed
+    `--set full` summaries, tagged with the source hash they were taken on and
+    whether the current sources still match (else the figure is stale)."""
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        t = json.load(open(tp))
+    except Exception:
+        return None, None
+    meta = t.get("_meta", {})
+    v = t.get("values", t).get(key)
+    if v is None or isinstance(v, dict):
+        return None, None
+    src = {"file": "profiles/traffic.json", "profile": meta.get("source"),
+           "csrc_sha256_profiled": meta.get("csrc_sha256"), "csrc_sha256_now": csrc_sha256()}
+    src["stale"] = src["csrc_sha256_profiled"] != src["csrc_sha256_now"]
+    return float(v), src
+
+
+def relaunch_cmd(argv, n: int, port: int):
+    """The command that runs this bench as n ranks, one per GPU, the way the
+    driver launches it (torch.distributed.run, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__)] + list(argv)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 
 
 def oracle_step(blk: np.ndarray, om, oluts, mode: str):
@@ -119,6 +166,49 @@ def oracle_rows_per_s(A_host: np.ndarray, om, oluts, budget_s: float, mode: str)
         rows += blk.shape[0]
         i += 1
     return rows / t_tot, rows, t_tot
+
+
+def rank_parity(A, out, codes, model_blob, B, name, mode, op, col, pq, rank, n_rows):
+    """Verification leg, outside the timed region: n_rows rows of THIS rank's
+    shard (seeded random rows + the shard's last 64) recomputed by the oracle
+    and compared with what the timed launches wrote -- codes and fp32 outputs
+    bit for bit (PQ codes: the Eq. pqLoss validity rule)."""
+    import torch
+    import oracle as O
+    from datagen.synth import CONFIGS
+    spec = CONFIGS[name]
+    n = out.shape[0] if op != "encode" else codes.shape[0]
+    g = np.random.default_rng([7, rank])
+    k = min(n, n_rows)
+    tail = np.arange(max(0, n - 64), n)
+    rnd = g.choice(max(1, n - 64), size=max(0, min(k - len(tail), n - 64)), replace=False)
+    idx = np.unique(np.concatenate([rnd, tail])).astype(np.int64)
+    ti = torch.from_numpy(idx).to(A.device)
+    rows = (A.index_select(1, ti).t() if col else A.index_select(0, ti)).cpu().numpy()
+    om = O.read_model(model_blob)
+    oluts = O.make_luts(om, B, mode, spec.U) if op != "encode" else None
+    if pq:
+        ref_codes = None
+        ok_codes, why = O.check_pq_codes(rows, om, O.unpack_codes(
+            codes.index_select(0, ti).cpu().numpy(), spec.C))
+    else:
+        ref_codes = O.encode_u8(rows, om) if rows.dtype == np.uint8 else O.encode(rows, om)
+        ok_codes, why = True, ""
+    mism = 0
+    if op == "encode":
+        if ref_codes is not None:
+            got = codes.index_select(0, ti).cpu().numpy()
+            mism = int((got != O.pack_codes(ref_codes)).any(axis=1).sum())
+    else:
+        src = ref_codes
+        if pq:   # PQ scan of the GPU's (validated) codes
+            src = O.unpack_codes(codes.index_select(0, ti).cpu().numpy(), spec.C)
+        S = O.scan_exact(src, oluts.Tq) if mode == "exact" else O.scan_avg(src, oluts.Tq, oluts.U)
+        ref = O.dequantize(S, oluts.alpha, oluts.beta32)
+        got = out.index_select(0, ti).cpu().numpy()
+        mism = int((got.view(np.int32) != ref.view(np.int32)).any(axis=1).sum())
+    return {"rows": int(len(idx)), "mismatched_rows": mism, "codes_valid": bool(ok_codes),
+            "ok": bool(mism == 0 and ok_codes), "detail": why}
 
 
 def _metric(name):
@@ -207,7 +297,11 @@ def run_reference(args):
     oluts = O.make_luts(om, _config_B(name), args.mode, spec.U)
     sample = 1 << 16
     if spec.kind == "relu":
-        A = relu_lowrank_torch(relu_W(name), sample, 0, "cpu").numpy()
+        # the GPU arm's own rows: the bench generator runs on the device (its
+        # CUDA RNG stream), then the rows come to the host
+        import torch
+        gen_dev = "cuda" if torch.cuda.is_available() else "cpu"
+        A = relu_lowrank_torch(relu_W(name), sample, 0, gen_dev).cpu().numpy()
     else:
         A = make_config_data(name, n_test=sample, n_train=0)[1]
     rows_per_step = ORACLE_CHUNK
@@ -224,10 +318,12 @@ def run_reference(args):
         "impl": "reference", "metric": _metric(name), "value": value, "unit": "rows/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8" if A.dtype == np.uint8 else "fp32", "data": "synthetic",
         "config": {"workload": f"{name} (D={spec.D}, M={spec.M}, C={spec.C}), {args.mode} sum; "
-                   "oracle on 16384-row steps from the same generator",
-                   "rows_per_step": rows_per_step},
+                   "oracle on 16384-row steps of the GPU arm's first rows",
+                   "rows_per_step": rows_per_step,
+                   "rows_generated_on": gen_dev if spec.kind == "relu" else "host (image patches)"},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": 1, "kind": "oracle",
                          "sample": f"{args.steps} steps x 16384 rows of the bench generator"},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -420,6 +516,23 @@ def run(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # --- per-rank parity of this rank's shard against the oracle (untimed) ----
+    par = None
+    if args.parity_rows > 0:
+        par = rank_parity(A, out, codes, model_blob, _config_B(name), args.mode, op, col, pq,
+                          rank, args.parity_rows)
+        if ws > 1:
+            flags = [None] * ws
+            dist.all_gather_object(flags, par)
+            par = {"rows_per_rank": par["rows"], "ranks": ws,
+                   "ranks_ok": sum(f["ok"] for f in flags),
+                   "mismatched_rows": sum(f["mismatched_rows"] for f in flags),
+                   "ok": all(f["ok"] for f in flags)}
+        else:
+            par = {"rows_per_rank": par["rows"], "ranks": 1, "ranks_ok": int(par["ok"]),
+                   "mismatched_rows": par["mismatched_rows"], "ok": par["ok"]}
+        par["what"] = ("seeded random rows + the last 64 of every rank's shard, oracle "
+                       "(oracle/) vs the launch outputs, bit for bit")
     clk = _clock_sampler(dev) if rank == 0 else None
     time.sleep(0.3 if clk else 0)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -438,7 +551,19 @@ def run(args):
     per_launch = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     elapsed_ms = ev[0].elapsed_time(ev[-1])
     clocks = _clock_summary(clk, t_wall0, t_wall1)
-    elapsed_ms = allreduce_max(elapsed_ms)
+    elapsed_ms = allreduce_max(elapsed_ms)       # the slowest rank's timed region
+    # The paper's protocol: 5 trials, each the best of 20
+    # executions. With fewer than 100 timed steps the missing executions run
+    # here, after the declared region, each bracketed by its own events.
+    proto_ms = list(per_launch[:100])
+    if len(proto_ms) < 100:
+        pe = [torch.cuda.Event(enable_timing=True) for _ in range(100 - len(proto_ms) + 1)]
+        pe[0].record(stream)
+        for i in range(len(pe) - 1):
+            step()
+            pe[i + 1].record(stream)
+        torch.cuda.synchronize()
+        proto_ms += [pe[i].elapsed_time(pe[i + 1]) for i in range(len(pe) - 1)]
 
     rows_total = n * ws * args.steps
     value = rows_total / (elapsed_ms / 1e3)
@@ -467,21 +592,22 @@ def run(args):
         probe = {"gbs": n * bytes_per_row / t_probe / 1e9,
                  "what": "plain streaming kernel, same bytes (read A, write M floats/row), no tables"}
     peak, peak_kind = _peaks()
-    avg_launch_s = statistics.mean(per_launch) / 1e3
-    # The paper's protocol: a trial = best of 20
-    # executions; report the median and spread of the trials. Derived from the
-    # same per-launch CUDA-event times (consecutive groups of 20 launches).
-    proto = None
-    if args.steps >= 20:
-        trials = [n / (min(per_launch[i:i + 20]) / 1e3) for i in range(0, args.steps - 19, 20)]
-        proto = {"trials": len(trials), "best_of": 20, "median_rows_per_s": statistics.median(trials),
-                 "std_rows_per_s": statistics.pstdev(trials) if len(trials) > 1 else 0.0}
+    # Per-GPU launch time = the slowest rank's timed region / steps (one launch
+    # per step): `achieved` is per GPU against the per-GPU peak; the aggregate
+    # (x ws) is reported beside it. On one GPU this is the mean launch time.
+    avg_launch_s = elapsed_ms / args.steps / 1e3
+    trials = [n / (min(proto_ms[i:i + 20]) / 1e3) for i in range(0, 100, 20)]
+    proto = {"trials": len(trials), "best_of": 20, "median_rows_per_s": statistics.median(trials),
+             "std_rows_per_s": statistics.pstdev(trials), "per": "gpu (rank 0)",
+             "launches": ("the timed steps" if args.steps >= 100 else
+                          f"{args.steps} timed + {100 - args.steps} untimed after the region")}
     achieved_gbs = n * bytes_per_row / avg_launch_s / 1e9
     alu_roof = None
     if pq:
-        # The PQ encoder is bound by the fp32 pipe, not HBM: 16 prototypes x D
-        # dims x (subtract, multiply, add) per row (Eq. pqLoss, no FMA).
-        # Peak (derived): 148 SMs x 128 fp32 lanes x 1 op/clk x max clock.
+        # The PQ encoder (expanded form ||p||^2 - 2<a,p>, reading P1) does
+        # 16 prototypes x D dims FMAs per row (2 flops each) against the fp32
+        # pipe (derived: 148 SMs x 128 lanes x 2 flops x clock) and
+        # reads 4 D bytes of A per row: report the nearer roofline.
         pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         torch.cuda.synchronize()
         pe[0].record(stream)
@@ -491,12 +617,21 @@ def run(args):
         torch.cuda.synchronize()
         t_enc = pe[0].elapsed_time(pe[1]) / 1e3 / args.steps
         sm_mhz = (clocks or {}).get("sm_max_mhz") or 1965.0
-        fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
-        tflops = n * 48 * spec.D / t_enc / 1e12
-        alu_roof = {"bound": "alu", "achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s",
-                   "frac": tflops / fp32_peak, "peak_kind": "derived: 148 SMs x 128 fp32 lanes x clock",
-                   "traffic": None, "algorithmic_flops_per_launch": n * 48 * spec.D,
-                   "kernel": "k_encode_pq", "encode_rows_per_s": n / t_enc}
+        fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+        tflops = n * 32 * spec.D / t_enc / 1e12
+        enc_gbs = n * (4 * spec.D + (spec.C + 1) // 2) / t_enc / 1e9
+        fma = {"bound": "alu", "achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+               "frac": tflops / fp32_peak,
+               "peak_kind": "derived: 148 SMs x 128 fp32 lanes x 2 flops (FMA) x clock",
+               "traffic": None, "algorithmic_flops_per_launch": n * 32 * spec.D}
+        hbm = {"bound": "hbm", "achieved": enc_gbs, "peak": peak, "unit": "GB/s",
+               "frac": enc_gbs / peak, "peak_kind": peak_kind, "traffic": None,
+               "algorithmic_bytes_per_launch": n * (4 * spec.D + (spec.C + 1) // 2)}
+        near = max((fma, hbm), key=lambda r: r["frac"])
+        other = hbm if near is fma else fma
+        alu_roof = dict(near)
+        alu_roof.update(kernel="k_encode_pq", encode_rows_per_s=n / t_enc,
+                        other_roofline={k: other[k] for k in ("bound", "achieved", "peak", "unit", "frac")})
 
     if op == "scan" and not pq:
         # Unfused mdn_scan moves (C/2 + 4M) B/row but does C*M table-byte
@@ -662,7 +797,8 @@ def run(args):
 
     # --- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only ---
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and op == "amm" and not col and not pq:
+    # (at N > 1 rank 0 runs it after every rank's timed region; the others wait)
+    if rank == 0 and not args.no_cpu_baseline and op == "amm" and not col and not pq:
         import oracle as O
         om = O.read_model(model_blob)
         oluts = O.make_luts(om, B, args.mode, spec.U)
@@ -695,18 +831,15 @@ def run(args):
                             "names": sorted({n.split("(")[0][:80] for n in names})}
         except Exception as e:  # pragma: no cover - profiler unavailable
             prof_kernels = {"error": str(e)[:200]}
+    if ws > 1:
+        dist.barrier()                 # rank 0's CPU legs ran after every timed region
     if rank == 0:
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            try:
-                key = (f"{name}{'_col' if col else ''}{'' if op == 'amm' else '_' + op}"
-                       f"{'_pq' if pq else ''}_{args.mode}")
-                traffic = json.load(open(tp)).get(key)
-            except Exception:
-                traffic = None
+        key = (f"{name}{'_col' if col else ''}{'' if op == 'amm' else '_' + op}"
+               f"{'_pq' if pq else ''}_{args.mode}")
+        traffic, traffic_src = traffic_lookup(key)
         if alu_roof is not None and alu_roof.get("traffic") is None and traffic is not None:
             alu_roof["traffic"] = traffic          # ncu DRAM bytes of this op's kernel
+            alu_roof["traffic_source"] = traffic_src
         line = {
             "metric": _metric(name) + ("" if op == "amm" else f" [{op} only]")
                       + (" [column-major A]" if col else "") + (" [PQ encoder]" if pq else ""),
@@ -714,7 +847,11 @@ def run(args):
             "unit": "rows/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
-            "vs_baseline": None, "dtype": "u8",
+            "vs_baseline": None,
+            # the arithmetic type of the path: fp32 A (fp32 compares, fp32
+            # dequantised output; u8 tables, int32 sums) or 8-bit A (integer
+            # compares)
+            "dtype": "u8" if u8 else "fp32",
             "data": "synthetic",
             "config": {"workload": f"{name}: D={spec.D}, M={spec.M}, C={spec.C}, K=16, {args.mode} sum"
                        + (f" (U={spec.U})" if args.mode == "avg" else "")
@@ -723,13 +860,18 @@ def run(args):
                           if pq else ", oracle-trained trees / ridge prototypes")
                        + ("; A stored column-major (At = A^T), only the split columns read" if col else ""),
                        "rows_per_gpu": n, "global_rows_per_step": n * ws,
-                       "A_bytes_per_gpu": n * 4 * spec.D,
-                       "l2": f"inputs {n * 4 * spec.D / 2**30:.1f} GiB per GPU > 126 MB L2; no flush",
+                       "A_dtype": "u8" if u8 else "fp32", "lut_dtype": "u8",
+                       "sum_dtype": "int32 (16-bit SWAR lanes)", "out_dtype": "fp32",
+                       "A_bytes_per_gpu": n * ea * spec.D,
+                       "l2": f"inputs {n * ea * spec.D / 2**30:.2f} GiB per GPU > 126 MB L2; no flush",
                        "parallelism": f"row-sharded dp{ws}, model+LUT NCCL broadcast once"},
             "pct_hbm_nominal_8tbs": achieved_gbs / NOMINAL_HBM_GBS,
             "roofline": alu_roof or {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "peak_kind": peak_kind,
-                         "traffic": traffic,
+                         "per": "gpu (slowest rank's launch time)",
+                         "aggregate_achieved": achieved_gbs * ws,
+                         "aggregate_peak": peak * ws,
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": n * bytes_per_row,
                          "kernel": (("ws_cm_gather4" if spec.C >= 16 else "k_amm_cm") if col
                                     else ("pq" if pq else mdn.mdn_amm_variant(model, luts, spec.D)))
@@ -737,6 +879,7 @@ def run(args):
                          "frac_of_stream_probe": (achieved_gbs / probe["gbs"]) if probe else None},
             "stream_probe": probe,
             "protocol_p378": proto,
+            "parity": par,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * (2 if pq and op == "amm" else 1),
@@ -752,7 +895,7 @@ def run(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
-    return 0
+    return 0 if (par is None or par["ok"]) else 1
 
 
 def main():
@@ -777,7 +920,21 @@ def main():
                     help="row-major A (default) or column-major A (SURVEY N2: split-column gather)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--parity-rows", type=int, default=PARITY_ROWS,
+                    help="rows of each rank's shard checked against the oracle before timing")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: run as N ranks, one per
+        # GPU, exactly as the driver's torchrun launch does.
+        cmd = relaunch_cmd(sys.argv[1:], args.gpus, _free_port())
+        print("bench.py: launching " + " ".join(cmd[1:6]) + " ...", file=sys.stderr, flush=True)
+        return subprocess.call(cmd)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws_env} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     if args.op == "train":

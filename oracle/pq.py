@@ -13,11 +13,19 @@ methods") can be reproduced in shape on B200. Restated from Sec. 3 (L132-190):
       outside J^(c), App. A quantisation, exact or averaging scan).
 
 Readings (DESIGN.md):
-  P1  Floating point decides the integer code, so the distance is evaluated
-      in the precision and order the GPU kernel uses: fp32, each operation
-      rounded separately (t = a_j - p, t*t, running sum; no fused multiply-
-      add), j ascending within J^(c). The plain fp64 definition agrees except
-      where two distances are within that rounding error (pinned in tests).
+  P1  Floating point decides the integer code. The oracle evaluates Eq.
+      pqLoss as written, in fp64 (pq_distances), and its code is the first
+      argmin (encode_pq). An implementation that evaluates the distance in
+      fp32 -- in any order, with fused multiply-adds, or in the argmin-
+      invariant expanded form ||p||^2 - 2<a,p> (||a||^2 is the same for every
+      k) -- may pick another prototype only when the two are closer than its
+      rounding can resolve: check_pq_codes accepts code k iff
+          d64(k) <= d64(k*) + eps(k) + eps(k*),   k* the first fp64 argmin,
+      eps(k) = gamma_{2d+4} * (sum_j (a_j - p_kj)^2 + sum_j p_kj^2
+                               + 2 sum_j |a_j p_kj|),
+      gamma_n = n u / (1 - n u), u = 2^-24 (the standard bound on an n-term
+      fp32 dot product / sum of squares, covering both forms). Outside that
+      margin the code must be k*.
   P2  argmin ties -> the lowest k.
   P3  K-means (not specified beyond "K-means"): Lloyd iterations from a
       seeded k-means++ initialisation, fp64 arithmetic, a fixed iteration
@@ -79,21 +87,35 @@ def train_pq(A_train: np.ndarray, C: int, n_iter: int = 25, seed: int = 0,
 
 
 def pq_distances(A: np.ndarray, model: Model, c: int) -> np.ndarray:
-    """sum_{j in J^(c)} (a_j - P_kj)^2 for every row and k, in fp32 with each
-    operation rounded separately, j ascending (reading P1). (N, K) float32."""
-    A = np.asarray(A, np.float32)
+    """Eq. pqLoss (L182-184) as written: sum_{j in J^(c)} (a_j - P_kj)^2 for
+    every row and k, in fp64 (reading P1). (N, K) float64."""
+    A = np.asarray(A, np.float32).astype(np.float64)
     b, e = model.sub[c]
-    proto = model.P[K * c:K * (c + 1), b:e].astype(np.float32)     # (K, d)
-    dist = np.zeros((A.shape[0], K), np.float32)
-    for j in range(e - b):
-        t = A[:, b + j, None] - proto[None, :, j]                  # fp32 subtract
-        dist = dist + t * t                                        # fp32 mul, fp32 add
-    return dist
+    proto = model.P[K * c:K * (c + 1), b:e].astype(np.float64)     # (K, d)
+    return ((A[:, None, b:e] - proto[None, :, :]) ** 2).sum(2)
+
+
+def pq_rounding_bound(A: np.ndarray, model: Model, c: int) -> np.ndarray:
+    """eps(k) of reading P1 for every row and k: gamma_{2d+4} times the sum of
+    the magnitudes an fp32 evaluation of Eq. pqLoss accumulates, in either the
+    direct form (sum of squared differences) or the expanded form
+    (||p||^2 - 2 <a, p>). (N, K) float64."""
+    A = np.asarray(A, np.float32).astype(np.float64)
+    b, e = model.sub[c]
+    d = e - b
+    proto = model.P[K * c:K * (c + 1), b:e].astype(np.float64)
+    u = 2.0 ** -24
+    n = 2 * d + 4
+    gamma = n * u / (1 - n * u)
+    mag = (pq_distances(A, model, c) + (proto ** 2).sum(1)[None, :]
+           + 2 * np.abs(A[:, b:e]) @ np.abs(proto).T)
+    return gamma * mag
 
 
 def encode_pq(A: np.ndarray, model: Model) -> np.ndarray:
     """g(A) for PQ (Eq. pqLoss): per codebook the index of the
-    nearest prototype, ties to the lowest k (reading P2). (N, C) uint8."""
+    nearest prototype by the fp64 distance, ties to the lowest k (readings P1,
+    P2). (N, C) uint8."""
     if not getattr(model, "pq", False):
         raise ValueError("not a PQ model")
     codes = np.empty((np.asarray(A).shape[0], model.C), np.uint8)
@@ -102,9 +124,36 @@ def encode_pq(A: np.ndarray, model: Model) -> np.ndarray:
     return codes
 
 
-def amm_pq(A: np.ndarray, model: Model, luts):
-    """PQ codes through the same f and dequantisation as MADDNESS."""
+def check_pq_codes(A: np.ndarray, model: Model, codes: np.ndarray):
+    """Validity of another implementation's PQ codes (N, C) against Eq. pqLoss
+    (reading P1): every code's fp64 distance is within its rounding bound of
+    the minimum, which forces the first argmin wherever the margin exceeds the
+    bound. Returns (ok, detail)."""
+    if not getattr(model, "pq", False):
+        raise ValueError("not a PQ model")
+    codes = np.asarray(codes).astype(np.int64)
+    bad = differ = 0
+    for c in range(model.C):
+        dist = pq_distances(A, model, c)
+        eps = pq_rounding_bound(A, model, c)
+        kstar = dist.argmin(1)
+        r = np.arange(dist.shape[0])
+        k = codes[:, c]
+        valid = (k >= 0) & (k < K)
+        kk = np.where(valid, k, 0)
+        within = dist[r, kk] <= dist[r, kstar] + eps[r, kk] + eps[r, kstar]
+        bad += int((~(valid & within)).sum())
+        differ += int((k != kstar).sum())
+    return bad == 0, (f"{bad} codes outside the rounding bound; {differ} codes differ "
+                      f"from the first fp64 argmin (near-ties)")
+
+
+def amm_pq(A: np.ndarray, model: Model, luts, codes=None):
+    """PQ codes through the same f and dequantisation as MADDNESS; `codes`
+    (e.g. another implementation's codes, validated by check_pq_codes)
+    replace encode_pq's where given."""
     from .maddness import dequantize, scan_avg, scan_exact
-    codes = encode_pq(A, model)
+    if codes is None:
+        codes = encode_pq(A, model)
     S = scan_exact(codes, luts.Tq) if luts.mode == "exact" else scan_avg(codes, luts.Tq, luts.U)
     return codes, S, dequantize(S, luts.alpha, luts.beta32)

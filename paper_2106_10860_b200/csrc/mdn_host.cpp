@@ -253,16 +253,22 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
               256 % C == 0 && C % 2 == 0;
     for (uint32_t cc = 0; cc < C && eq; ++cc) eq = m->h_sub[cc] == DS * cc && m->h_sub_e[cc] == DS * (cc + 1);
     if (eq) {
+      // fast encoder operands of the expanded form ||p||^2 - 2 <a, p> (reading
+      // P1): q = -2 p (exact in fp32) in [k][j/4][c][4], then ||p_k||^2 of
+      // every (k, c) summed in fp64 and rounded once, [k][c]
       m->pq_ds = DS;
-      h_pqcent.resize((size_t)16 * D);
-      const float* Pf = reinterpret_cast<const float*>(P);
+      h_pqcent.assign((size_t)16 * D + 16 * C, 0.f);
       for (int k = 0; k < 16; ++k)
-        for (int j = 0; j < DS; ++j)
-          for (uint32_t cc = 0; cc < C; ++cc) {
+        for (uint32_t cc = 0; cc < C; ++cc) {
+          double pn = 0.0;
+          for (int j = 0; j < DS; ++j) {
             float v;
-            memcpy(&v, reinterpret_cast<const uint8_t*>(Pf) + (((size_t)(16 * cc + k) * D + cc * DS + j) * 4), 4);
-            h_pqcent[(((size_t)k * (DS / 4) + j / 4) * C + cc) * 4 + (j % 4)] = v;
+            memcpy(&v, P + (((size_t)(16 * cc + k) * D + cc * DS + j) * 4), 4);
+            h_pqcent[(((size_t)k * (DS / 4) + j / 4) * C + cc) * 4 + (j % 4)] = -2.0f * v;
+            pn += (double)v * (double)v;
           }
+          h_pqcent[(size_t)16 * D + (size_t)k * C + cc] = (float)pn;
+        }
     }
   }
 

@@ -5,16 +5,20 @@
 // K-means (L155-163; oracle/pq.py). The codes use the same 4-bit packing as
 // mdn_encode and feed the same mdn_scan / tables (h(B) from the dense P).
 //
-// Floating point decides the integer code, so the distance is evaluated in the
-// order and precision the oracle uses (reading P1): fp32, every
-// subtract / multiply / add rounded separately (__fsub_rn / __fmul_rn /
-// __fadd_rn, no FMA contraction), j ascending; ties go to the lowest k.
+// Floating point decides the integer code. The oracle takes the first argmin
+// of the fp64 definition; this kernel evaluates the argmin-invariant expanded
+// form e_k = ||p_k||^2 - 2 <a, p_k> (||a||^2 is common to every k) in fp32
+// with fused multiply-adds, and DESIGN.md reading P1 accepts its code iff the
+// code's fp64 distance is within the fp32 rounding bound of the minimum
+// (oracle.check_pq_codes); ties go to the lowest k.
 //
 // k_encode_pq<DS, R>: a thread owns one codebook c (lane % C) and R rows; the
-// 16 x DS prototypes of c are read from shared memory (layout [k][j/4][c][4]:
-// one conflict-free LDS.128 per 4 dims, reused for the R rows), so the kernel
-// is bound by the fp32 pipe: 3 * 16 * D flops per row (cls100: 24,576), not
-// by HBM -- which is the point of the comparison (Sec. 5.1).
+// 16 x DS scaled prototypes q = -2 p of c are read from shared memory (layout
+// [k][j/4][c][4]: one conflict-free LDS.128 per 4 dims, reused for the R
+// rows) next to ||p_k||^2 ([k][c]); one FFMA per (row, prototype, dim), two
+// accumulator chains per row: 16 D FMAs per row (cls100: 8,192), so the
+// kernel is bound by HBM (4 D bytes per row) or by the fp32 pipe, whichever
+// is nearer (Sec. 5.1).
 #include <cuda_runtime.h>
 
 #include "mdn_internal.h"
@@ -32,10 +36,11 @@ __global__ void __launch_bounds__(THREADS) k_encode_pq(const float* __restrict__
                                                        const float4* __restrict__ cent_g,
                                                        uint8_t* __restrict__ codes) {
   extern __shared__ __align__(16) unsigned char smem[];
-  float4* s_cent = reinterpret_cast<float4*>(smem);             // [16][DS/4][C]
-  const int n4 = 16 * (DS / 4) * C;
+  float4* s_cent = reinterpret_cast<float4*>(smem);             // [16][DS/4][C] of -2 p
+  const int n4 = 16 * (DS / 4) * C + 4 * C;                     // + ||p||^2 [16][C]
   for (int i = threadIdx.x; i < n4; i += blockDim.x) s_cent[i] = cent_g[i];
   __syncthreads();
+  const float* s_pn = reinterpret_cast<const float*>(s_cent + 16 * (DS / 4) * C);
   const int c = threadIdx.x % C;
   const int rg = threadIdx.x / C;
   const int groups_per_block = THREADS / C;
@@ -61,24 +66,26 @@ __global__ void __launch_bounds__(THREADS) k_encode_pq(const float* __restrict__
     for (int r = 0; r < R; ++r) best[r] = __int_as_float(0x7f800000), bk[r] = 0u;   // +inf
 #pragma unroll 1
     for (int k = 0; k < 16; ++k) {
-      float d[R];
+      float d0[R], d1[R];
+      const float pn = s_pn[k * C + c];
 #pragma unroll
-      for (int r = 0; r < R; ++r) d[r] = 0.f;
+      for (int r = 0; r < R; ++r) d0[r] = pn, d1[r] = 0.f;
 #pragma unroll
       for (int j4 = 0; j4 < DS / 4; ++j4) {
-        const float4 p = s_cent[(k * (DS / 4) + j4) * C + c];
-        const float pv[4] = {p.x, p.y, p.z, p.w};
+        const float4 q = s_cent[(k * (DS / 4) + j4) * C + c];
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const float t = __fsub_rn(x[r][4 * j4 + jj], pv[jj]);
-            d[r] = __fadd_rn(d[r], __fmul_rn(t, t));
-          }
+        for (int r = 0; r < R; ++r) {
+          d0[r] = __fmaf_rn(x[r][4 * j4], q.x, d0[r]);
+          d1[r] = __fmaf_rn(x[r][4 * j4 + 1], q.y, d1[r]);
+          d0[r] = __fmaf_rn(x[r][4 * j4 + 2], q.z, d0[r]);
+          d1[r] = __fmaf_rn(x[r][4 * j4 + 3], q.w, d1[r]);
+        }
       }
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (d[r] < best[r]) best[r] = d[r], bk[r] = (uint32_t)k;   // strict: ties keep the lowest k
+      for (int r = 0; r < R; ++r) {
+        const float d = __fadd_rn(d0[r], d1[r]);
+        if (d < best[r]) best[r] = d, bk[r] = (uint32_t)k;     // strict: ties keep the lowest k
+      }
     }
     // pack two codes per byte: low nibble = even codebook (L147, L608)
 #pragma unroll
@@ -125,7 +132,7 @@ template <int DS, int R>
 cudaError_t launch(const float* A, int64_t N, int64_t lda, int C, const float* cent,
                    uint8_t* codes, cudaStream_t s) {
   auto k = k_encode_pq<DS, R>;
-  const size_t smem = (size_t)16 * DS * C * 4;
+  const size_t smem = ((size_t)16 * DS * C + 16 * C) * 4;
   cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -146,14 +153,14 @@ cudaError_t launch(const float* A, int64_t N, int64_t lda, int C, const float* c
 
 using namespace fast::pq;
 
-// t.pq_cent: [16][DS/4][C][4] prototypes when every subspace is [c DS, (c+1) DS)
+// t.pq_cent: [16][DS/4][C][4] scaled prototypes -2 p, then ||p||^2 [16][C], when every subspace is [c DS, (c+1) DS)
 // with DS in {4, 8, 16, 32} and THREADS % C == 0 (else null: generic kernel).
 cudaError_t launch_encode_pq(const TreesDev& t, const float* P_dense, const uint16_t* sub_b,
                              const uint16_t* sub_e, const float* A, int64_t N, int64_t lda,
                              uint8_t* codes, cudaStream_t s) {
   const bool fast_ok = t.pq_cent && t.pq_ds > 0 && (reinterpret_cast<uintptr_t>(A) & 15u) == 0 &&
                        lda % 4 == 0 && t.C % 2 == 0 &&
-                       (size_t)16 * t.pq_ds * t.C * 4 <= (size_t)fast::dev_info().smem_optin;
+                       ((size_t)16 * t.pq_ds * t.C + 16 * t.C) * 4 <= (size_t)fast::dev_info().smem_optin;
   if (fast_ok) {
     switch (t.pq_ds) {
       case 4: return launch<4, 8>(A, N, lda, t.C, t.pq_cent, codes, s);

@@ -87,7 +87,7 @@ def main():
         codes = torch.empty((333, 8), dtype=torch.uint8, device="cuda")
         mdn.mdn_encode_pq(model, torch.from_numpy(A).cuda(), codes)
         torch.cuda.synchronize()
-        if not (codes.cpu().numpy() == O.pack_codes(O.encode_pq(A, om))).all():
+        if not O.check_pq_codes(A, om, O.unpack_codes(codes.cpu().numpy(), om.C))[0]:
             print("MISMATCH pq")
             BAD.append("pq")
     # GPU training (small)

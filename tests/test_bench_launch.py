@@ -1,0 +1,50 @@
+"""bench.py's launch contract (CPU): `--gpus N` without a launcher re-runs the
+bench as N ranks under torch.distributed.run on 127.0.0.1; a WORLD_SIZE that
+disagrees with --gpus is an error; the ncu traffic figure is tied to the
+kernel sources it was measured on. The 2-rank run itself is a -m gpu test
+(test_gpu_bench.py)."""
+import json
+import os
+import subprocess
+import sys
+
+from helpers import ROOT
+
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+
+
+def test_relaunch_cmd_is_torchrun_on_localhost():
+    cmd = bench.relaunch_cmd(["--gpus", "4", "--steps", "7"], 4, 29555)
+    assert cmd[:3] == [sys.executable, "-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+    assert "--master-port=29555" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "7"]
+    assert os.path.samefile(cmd[-5], os.path.join(ROOT, "bench.py"))
+
+
+def test_world_size_mismatch_fails():
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 2
+    assert "WORLD_SIZE=3" in p.stderr
+
+
+def test_traffic_lookup_tags_source_hash(tmp_path, monkeypatch):
+    h = bench.csrc_sha256()
+    assert len(h) == 16
+    v, src = bench.traffic_lookup("cls100_exact")
+    if v is not None:
+        assert src["csrc_sha256_now"] == h
+        assert src["stale"] == (src["csrc_sha256_profiled"] != h)
+    # a figure measured on other sources is reported stale
+    d = tmp_path / "profiles"
+    d.mkdir()
+    (d / "traffic.json").write_text(json.dumps(
+        {"_meta": {"csrc_sha256": "0" * 16, "source": "x"}, "values": {"k_exact": 5.0}}))
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    monkeypatch.setattr(bench, "csrc_sha256", lambda: h)
+    v, src = bench.traffic_lookup("k_exact")
+    assert v == 5.0 and src["stale"]
+    assert bench.traffic_lookup("missing") == (None, None)

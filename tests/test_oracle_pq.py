@@ -1,8 +1,10 @@
 """Pins for the PQ comparator oracle (Sec. 3).
 
-encode_pq follows Eq. pqLoss (L182-184) in fp32 with separately rounded
-operations (reading P1); these tests tie it to the fp64 definition, to exact
-hits and hand-placed grids, and K-means to its defining properties."""
+encode_pq is Eq. pqLoss (L182-184) in fp64, first argmin (readings P1, P2);
+these tests tie it to exact hits, hand-placed grids, the 1-D Voronoi closed
+form and translation / permutation invariance; the rounding bound of P1 to
+two real fp32 evaluations; check_pq_codes to what it must accept and reject;
+and K-means to its defining properties."""
 import numpy as np
 
 import oracle as O
@@ -18,26 +20,110 @@ def _random_pq_model(rng, C, d, scale=1.0):
                    thr=np.zeros((C, 15), np.float32), P=P, ridge=False, lam=0.0, pq=True)
 
 
-def test_encode_pq_matches_fp64_definition_off_ties():
-    """argmin_k sum_j (a_j - P_kj)^2 in fp64 (the plain definition) equals the
-    fp32 oracle wherever the best and second-best fp64 distances differ by more
-    than the fp32 evaluation error can move them."""
+def _fp32_direct(A, m, c):
+    """An fp32 implementation of Eq. pqLoss: subtract, multiply, add each
+    rounded, j ascending (no FMA)."""
+    b, e = m.sub[c]
+    P = m.P[16 * c:16 * (c + 1), b:e].astype(np.float32)
+    d = np.zeros((A.shape[0], 16), np.float32)
+    for j in range(e - b):
+        t = A[:, b + j, None].astype(np.float32) - P[None, :, j]
+        d = d + t * t
+    return d
+
+
+def _fp32_expanded(A, m, c):
+    """Another fp32 implementation: ||p||^2 (rounded once) + sum_j a_j (-2 p_j),
+    accumulated in fp32 -- the argmin-invariant form a fast kernel uses."""
+    b, e = m.sub[c]
+    P = m.P[16 * c:16 * (c + 1), b:e]
+    acc = np.broadcast_to((P.astype(np.float64) ** 2).sum(1).astype(np.float32),
+                          (A.shape[0], 16)).copy()
+    for j in range(e - b):
+        acc = acc + A[:, b + j, None].astype(np.float32) * (np.float32(-2) * P[None, :, j])
+    return acc
+
+
+def test_rounding_bound_covers_fp32_evaluations():
+    """eps(k) of reading P1 bounds the actual error of both fp32 forms against
+    the fp64 definition, on every row and prototype (incl. large offsets that
+    make the expanded form cancel)."""
     rng = np.random.default_rng(40)
+    for C, d, shift in ((4, 8, 0.0), (8, 4, 0.0), (3, 16, 0.0), (2, 32, 50.0)):
+        m = _random_pq_model(rng, C, d)
+        m.P[:] += np.float32(shift) * (m.P != 0)
+        A = (shift + rng.standard_normal((3000, C * d))).astype(np.float32)
+        for c, (b, e) in enumerate(m.sub):
+            d64 = O.pq_distances(A, m, c)
+            eps = O.pq_rounding_bound(A, m, c)
+            an = (A[:, b:e].astype(np.float64) ** 2).sum(1)[:, None]
+            assert (np.abs(_fp32_direct(A, m, c) - d64) <= eps).all()
+            assert (np.abs(_fp32_expanded(A, m, c).astype(np.float64) + an - d64) <= eps).all()
+
+
+def test_check_pq_codes_accepts_fp32_and_rejects_wrong_codes():
+    """fp32 argmins (either form) pass check_pq_codes; off near-ties they are
+    the fp64 first argmin; replacing a code by the second-best prototype where
+    the margin exceeds the bound fails."""
+    rng = np.random.default_rng(46)
     for C, d in ((4, 8), (8, 4), (3, 16)):
         m = _random_pq_model(rng, C, d)
         A = rng.standard_normal((4000, C * d)).astype(np.float32)
-        got = O.encode_pq(A, m)
-        for c, (b, e) in enumerate(m.sub):
-            X = A[:, b:e].astype(np.float64)
-            Pc = m.P[16 * c:16 * (c + 1), b:e].astype(np.float64)
-            dist = ((X[:, None, :] - Pc[None]) ** 2).sum(2)
-            srt = np.sort(dist, 1)
-            margin = srt[:, 1] - srt[:, 0]
-            # bound on the fp32 error of each distance: ~ (d + 2) ulp of the sum
-            tol = (e - b + 2) * np.finfo(np.float32).eps * 4 * srt[:, 1]
-            ok = margin > tol
-            assert ok.mean() > 0.99
-            assert (got[ok, c] == dist[ok].argmin(1)).all()
+        ref = O.encode_pq(A, m)
+        for form in (_fp32_direct, _fp32_expanded):
+            got = np.stack([form(A, m, c).argmin(1) for c in range(C)], 1)
+            ok, _ = O.check_pq_codes(A, m, got)
+            assert ok
+            assert (got != ref).mean() < 0.01
+        bad = ref.copy()
+        d64 = O.pq_distances(A, m, 0)
+        eps = O.pq_rounding_bound(A, m, 0)
+        second = np.argsort(d64, 1, kind="stable")[:, 1]
+        r = np.arange(len(A))
+        far = d64[r, second] - d64[r, ref[:, 0]] > 10 * (eps[r, second] + eps[r, ref[:, 0]])
+        assert far.any()
+        n0 = int(np.flatnonzero(far)[0])
+        bad[n0, 0] = second[n0]
+        assert not O.check_pq_codes(A, m, bad)[0]
+        bad[n0, 0] = 16                                 # out of range
+        assert not O.check_pq_codes(A, m, bad)[0]
+
+
+def test_encode_pq_one_dim_voronoi():
+    """C = 1, d = 1: the nearest of 16 sorted points on a line is the one whose
+    interval between neighbouring midpoints holds a (closed form)."""
+    rng = np.random.default_rng(47)
+    pts = np.sort(rng.uniform(-10, 10, 16)).astype(np.float32)
+    perm = rng.permutation(16)
+    P = pts[perm].reshape(16, 1)
+    m = O.Model(C=1, D=1, sub=[(0, 1)], dims=np.zeros((1, 4), np.int64),
+                thr=np.zeros((1, 15), np.float32), P=P, ridge=False, lam=0.0, pq=True)
+    a = rng.uniform(-12, 12, 5000).astype(np.float32)
+    mids = (pts[:-1].astype(np.float64) + pts[1:]) / 2
+    rank = np.searchsorted(mids, a.astype(np.float64))          # index into sorted points
+    keep = np.abs(a[:, None] - mids[None, :]).min(1) > 1e-4     # off the exact boundaries
+    want = np.argsort(perm)[rank]                                # sorted rank -> prototype index
+    got = O.encode_pq(a.reshape(-1, 1), m)[:, 0]
+    assert (got[keep] == want[keep]).all()
+
+
+def test_encode_pq_translation_and_permutation_invariance():
+    """Shifting rows and prototypes by the same vector keeps the codes;
+    permuting the prototypes permutes the codes."""
+    rng = np.random.default_rng(48)
+    m = _random_pq_model(rng, 4, 4)
+    A = rng.standard_normal((2000, 16)).astype(np.float32)
+    ref = O.encode_pq(A, m)
+    shift = np.float32(0.5)                                     # exact in fp32 at these magnitudes
+    m2 = _random_pq_model(rng, 4, 4)
+    m2.P[:] = m.P + shift * (m.P != 0)
+    assert (O.encode_pq(A + shift, m2) == ref).mean() > 0.999
+    perm = rng.permutation(16)
+    m3 = _random_pq_model(rng, 4, 4)
+    for c in range(4):
+        m3.P[16 * c:16 * (c + 1)] = m.P[16 * c + perm]
+    inv = np.argsort(perm)
+    assert (O.encode_pq(A, m3) == inv[ref]).all()
 
 
 def test_encode_pq_exact_hits_and_lowest_index_ties():
@@ -70,23 +156,6 @@ def test_encode_pq_hand_grid():
     idx = rng.integers(0, 16, 500)
     A = (P[idx] + rng.uniform(-4.9, 4.9, (500, 2))).astype(np.float32)
     assert (O.encode_pq(A, m)[:, 0] == idx).all()
-
-
-def test_pq_distances_literal_scalar_loop():
-    """The vectorised distances equal a literal scalar loop over j (fp32
-    subtract, multiply, add; j ascending) bit for bit."""
-    rng = np.random.default_rng(43)
-    m = _random_pq_model(rng, 2, 5)
-    A = rng.standard_normal((20, 10)).astype(np.float32)
-    for c, (b, e) in enumerate(m.sub):
-        got = O.pq_distances(A, m, c)
-        for n in range(20):
-            for k in range(16):
-                s = np.float32(0)
-                for j in range(b, e):
-                    t = np.float32(A[n, j]) - np.float32(m.P[16 * c + k, j])
-                    s = np.float32(s + np.float32(t * t))
-                assert got[n, k].view(np.uint32) == s.view(np.uint32)
 
 
 def test_kmeans_properties():
