@@ -428,6 +428,10 @@ def run(args):
     # single GPU (ranks never wait on each other's kernels); numbers from it
     # are not bench values. The real path is NCCL, one GPU per rank.
     backend = os.environ.get("MDN_DIST_BACKEND", "nccl")
+    if ws > 1 and backend == "nccl" and ws > torch.cuda.device_count():
+        print(f"bench.py: {ws} ranks need {ws} GPUs (NCCL, one GPU per rank); "
+              f"{torch.cuda.device_count()} visible", file=sys.stderr)
+        return 2
     if ws > 1:
         local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)

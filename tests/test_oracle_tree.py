@@ -77,3 +77,83 @@ def test_train_dims_inside_subspace():
     m = O.train(A, 3)
     for c, (b, e) in enumerate(m.sub):
         assert ((m.dims[c] >= b) & (m.dims[c] < e)).all()
+
+
+def test_select_idxs_hand_example_per_bucket_not_pooled():
+    """Alg. 2 line 2 (L265, L259): candidates rank by the loss summed over the
+    buckets, sum_B sum_{x in B} (x_j - mean_B x_j)^2, top 4 descending, ties to
+    the lower index (R3). Hand-computed values (2 buckets of 2 rows):
+
+        dim  bucket 0  bucket 1  per-bucket L  pooled SSE
+        0    0, 0      10, 10    0             100
+        1    0, 2      0, 2      2 + 2 = 4     4
+        2    0, 4      0, 0      8             12
+        3    1, 1      1, 1      0             0
+        4    0, 6      5, 5      18            22
+        5    0, 1      0, 1      0.5+0.5 = 1   1
+        6    0, 1      0, 1      1             1
+
+    per-bucket top 4 = {4, 2, 1, 5} (5 beats 6 on the tie); pooled would give
+    {0, 4, 2, 1}; the bottom 4 would give {0, 3, 5, 6}."""
+    cols = [((0, 0), (10, 10)), ((0, 2), (0, 2)), ((0, 4), (0, 0)), ((1, 1), (1, 1)),
+            ((0, 6), (5, 5)), ((0, 1), (0, 1)), ((0, 1), (0, 1))]
+    X = np.array([[c[0][0] for c in cols], [c[0][1] for c in cols],
+                  [c[1][0] for c in cols], [c[1][1] for c in cols]], np.float32)
+    buckets = [np.array([0, 1]), np.array([2, 3])]
+    assert O.heuristic_select_idxs(buckets, X) == [1, 2, 4, 5]
+    assert O.heuristic_select_idxs([np.arange(4)], X) == [0, 1, 2, 4]      # one bucket: pooled
+    assert O.heuristic_select_idxs(buckets, X[:, :3]) == [0, 1, 2]         # d < 4: all dims
+
+
+def _brute_split_loss(Xb: np.ndarray, j: int) -> float:
+    """min over every realisable split {x_j < v} / {x_j >= v} of the summed
+    two-pass SSE of both children over all dims (v at each distinct value of
+    x_j; v = the minimum puts every row right, which is the constant-column
+    case). Empty bucket -> 0."""
+    if Xb.shape[0] == 0:
+        return 0.0
+    best = np.inf
+    for v in np.unique(Xb[:, j]):
+        lo, hi = Xb[Xb[:, j] < v], Xb[Xb[:, j] >= v]
+        best = min(best, O.sse_two_pass(lo) + O.sse_two_pass(hi))
+    return best
+
+
+def test_add_tree_level_picks_first_bruteforce_argmin():
+    """Alg. 2 lines 4-15 (L281-293): the chosen dim minimises the bucket-summed
+    optimal split loss over the candidates, and is the FIRST (lowest-index)
+    minimiser (strict `<`, L289). Brute force over every realisable split,
+    on random relu / Gaussian data and at each level of a tree."""
+    rng = np.random.default_rng(10)
+    for it in range(40):
+        N, d = int(rng.integers(6, 60)), int(rng.integers(2, 9))
+        X = rng.standard_normal((N, d)).astype(np.float32)
+        if it % 2:
+            X = np.maximum(X, 0)
+        buckets = [np.arange(N)]
+        for t in range(3):
+            cands = O.heuristic_select_idxs(buckets, X)
+            tot = {j: sum(_brute_split_loss(X[b], j) for b in buckets) for j in cands}
+            new, l, j, v = O.add_tree_level(buckets, X)
+            lo = min(tot.values())
+            tol = 1e-9 * max(1.0, lo)
+            assert abs(l - lo) <= tol and abs(tot[j] - lo) <= tol
+            assert all(tot[jj] > lo + tol for jj in cands if jj < j), (tot, j)
+            buckets = new
+
+
+def test_add_tree_level_exact_tie_goes_to_lower_index():
+    """Two identical columns give bit-identical split losses: the lower index
+    must win (a `<=` at L289, or returning the last candidate, fails here);
+    with the better column in the middle of the candidates it must be found."""
+    rng = np.random.default_rng(11)
+    base = rng.standard_normal(64).astype(np.float32)
+    X = np.stack([rng.standard_normal(64) * 0.1, base, base, rng.standard_normal(64) * 0.1],
+                 1).astype(np.float32)
+    _, l, j, _ = O.add_tree_level([np.arange(64)], X)
+    assert j == 1
+    # the clear winner (two far clusters) in the middle of 4 candidates
+    Y = rng.standard_normal((64, 4)).astype(np.float32) * 0.1
+    Y[:, 2] += np.where(np.arange(64) < 32, -5.0, 5.0).astype(np.float32)
+    _, _, j, v = O.add_tree_level([np.arange(64)], Y)
+    assert j == 2 and -5 < v[0] < 5
