@@ -523,7 +523,7 @@ def run(args):
     # --- per-rank parity of this rank's shard against the oracle (untimed) ----
     par = None
     if args.parity_rows > 0:
-        par = rank_parity(A, out, codes, model_blob, _config_B(name), args.mode, op, col, pq,
+        par = rank_parity(A, out, codes, model_blob, _config_B(name), name, args.mode, op, col, pq,
                           rank, args.parity_rows)
         if ws > 1:
             flags = [None] * ws

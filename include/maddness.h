@@ -79,7 +79,7 @@ typedef struct mdn_exec mdn_exec;   /* host-buffer pipelined executor (e2e path)
 /* Parse a "model.mdnm v1" byte stream (host memory, `len` bytes) and upload
  * the split dims, thresholds and prototypes to `device`.
  * Errors: MDN_EFORMAT (with *err_off = offending byte offset; err_off may be
- * NULL), MDN_EVERSION, MDN_EINVAL (split dim >= D, C < 1, K != 16),
+ * NULL), MDN_EVERSION, MDN_EINVAL (split dim >= D, C < 1, K != 16, a NaN threshold),
  * MDN_ENOMEM, MDN_ECUDA. */
 int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out,
                    size_t* err_off);

@@ -202,6 +202,9 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
     for (int i = 0; i < 15; ++i) m->h_thr[c * THR_STRIDE + i] = r.get<float>();
     if (r.fail) return set_err(err_off, r.fail_off, MDN_EFORMAT);
     if (b > e || e > D) return set_err(err_off, rec, MDN_EFORMAT);
+    // a NaN threshold has no 8-bit split value and no meaning in Alg. 1
+    for (int i = 0; i < 15; ++i)
+      if (std::isnan(m->h_thr[c * THR_STRIDE + i])) return set_err(err_off, rec + 16 + 4 * i, MDN_EINVAL);
     for (int t = 0; t < 4; ++t) {
       if (m->h_dims[c * 4 + t] >= D) return set_err(err_off, rec + 8 + 2 * t, MDN_EINVAL);
       // split dims must lie in the codebook's subspace (reading R2)

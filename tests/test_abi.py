@@ -82,6 +82,17 @@ def test_model_parser_errors(lib):
     assert _load(lib, bytes(bad))[0] in (-1, -3)
 
 
+def test_model_nan_threshold_rejected(lib):
+    """A NaN threshold has no meaning in Alg. 1 (and no 8-bit split value):
+    MDN_EINVAL at its byte offset, before any device work."""
+    import numpy as np
+    import oracle as O
+    om = O.read_model(model_bytes("tiny"))
+    om.thr[2, 5] = np.nan
+    st, off = _load(lib, O.write_model(om))
+    assert st == -1 and off == 48 + 2 * 76 + 16 + 4 * 5
+
+
 def test_luts_parser_errors(lib):
     h, off = ct.c_void_p(), ct.c_size_t(0)
     lib.mdn_luts_load.argtypes = [ct.c_void_p, ct.c_size_t, ct.c_int, ct.POINTER(ct.c_void_p),
