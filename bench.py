@@ -577,24 +577,37 @@ def run(args):
     bytes_per_row = {"amm": a_bytes + 4 * spec.M, "encode": a_bytes + (spec.C + 1) // 2,
                      "scan": (spec.C + 1) // 2 + 4 * spec.M}[op]
 
-    # Achievable-bandwidth probe: a plain streaming kernel with the same byte
-    # mix (read A, write M floats per row), timed the same way.
+    # Achievable-bandwidth probe. For the general fused kernel (k_amm_ws) it
+    # is that kernel's own pipeline -- same TMA boxes, stages, grid, warp
+    # roles and stores -- with encode and scan removed (mdn_amm_probe); for the
+    # other variants a plain streaming kernel with the same byte mix.
     probe = None
-    if op == "amm" and not u8 and not col and not pq and spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
+    if op == "amm" and not u8 and not col and not pq:
         probe_out = torch.empty_like(out)     # never overwrite the step's output
-        for _ in range(2):
-            mdn.mdn_stream_probe(A, probe_out, stream=stream)
-        pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-        torch.cuda.synchronize()
-        pe[0].record(stream)
-        for _ in range(args.steps):
-            mdn.mdn_stream_probe(A, probe_out, stream=stream)
-        pe[1].record(stream)
-        torch.cuda.synchronize()
-        t_probe = pe[0].elapsed_time(pe[1]) / 1e3 / args.steps
+        variant = mdn.mdn_amm_variant(model, luts, spec.D)
+        if variant.startswith("ws"):
+            probe_fn = lambda: mdn.mdn_amm_probe(model, luts, A, probe_out, stream=stream)
+            what = ("mdn_amm_probe: the fused kernel's own pipeline (TMA boxes, stage/code rings, "
+                    "grid, warp roles, output stores) with encode and scan removed")
+        elif spec.D % 4 == 0 and (n * spec.M) % 4 == 0:
+            probe_fn = lambda: mdn.mdn_stream_probe(A, probe_out, stream=stream)
+            what = "plain streaming kernel, same bytes (read A, write M floats/row), no tables"
+        else:
+            probe_fn = None
+        if probe_fn is not None:
+            for _ in range(2):
+                probe_fn()
+            pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            torch.cuda.synchronize()
+            pe[0].record(stream)
+            for _ in range(args.steps):
+                probe_fn()
+            pe[1].record(stream)
+            torch.cuda.synchronize()
+            t_probe = allreduce_max(pe[0].elapsed_time(pe[1]) / 1e3 / args.steps)
+            probe = {"gbs": n * bytes_per_row / t_probe / 1e9, "rows_per_s_per_gpu": n / t_probe,
+                     "what": what}
         del probe_out
-        probe = {"gbs": n * bytes_per_row / t_probe / 1e9,
-                 "what": "plain streaming kernel, same bytes (read A, write M floats/row), no tables"}
     peak, peak_kind = _peaks()
     # Per-GPU launch time = the slowest rank's timed region / steps (one launch
     # per step): `achieved` is per GPU against the per-GPU peak; the aggregate

@@ -278,6 +278,16 @@ int mdn_encode_cm_host(mdn_exec* exec, const float* At_host, int64_t N, int64_t 
  * to the fused kernel's. */
 int mdn_stream_probe(const float* A, int64_t N, int64_t lda, int64_t D, float* out,
                      int64_t ldo, int64_t M, void* stream);
+/* Pipeline ceiling probe (not part of the method): the fused kernel that
+ * mdn_amm would launch for these arguments (the general warp-specialised
+ * k_amm_ws: same TMA boxes, stage ring, code ring, grid, warp roles and
+ * output stores) with Algorithm 1 and the table scan removed -- every output
+ * element is beta32. Its time is the achievable ceiling of mdn_amm's own data
+ * movement. Arguments, layouts and errors as mdn_amm; MDN_EINVAL also when
+ * mdn_amm would not use the general pipeline for these shapes (register-tree
+ * or generic kernels). */
+int mdn_amm_probe(const mdn_model* model, const mdn_luts* luts, const float* A, int64_t N,
+                  int64_t lda, float* out, int64_t ldo, void* stream);
 
 /* --------------------------------------------------------------- misc -- */
 

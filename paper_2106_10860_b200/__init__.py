@@ -53,6 +53,7 @@ _SIGS = {
     "mdn_abi_version": (_i32, []),
     "mdn_amm_variant": (_i32, [_vp, _vp, _i64, ct.c_char_p, _sz]),
     "mdn_stream_probe": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
+    "mdn_amm_probe": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "mdn_encode_u8": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "mdn_amm_u8": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "mdn_encode_cm": (_i32, [_vp, _vp, _i64, _i64, _vp, _vp]),
@@ -466,6 +467,18 @@ def mdn_stream_probe(A, out, stream=None):
     po = _dev_ptr(out, "float32", "out")
     _check(_lib.mdn_stream_probe(pa, A.shape[0], A.stride(0), A.shape[1], po, out.stride(0),
                                  out.shape[1], _stream_ptr(stream)), "mdn_stream_probe")
+    return out
+
+
+def mdn_amm_probe(model: Model, luts: Luts, A, out, stream=None):
+    """Diagnostics: mdn_amm's own pipeline with encode and scan removed (the
+    data-movement ceiling of the fused kernel); out = beta32 everywhere."""
+    pa = _dev_ptr(A, "float32", "A")
+    po = _dev_ptr(out, "float32", "out")
+    if out.shape != (A.shape[0], luts.M):
+        raise ValueError("out must be N x M")
+    _check(_lib.mdn_amm_probe(model._h, luts._h, pa, A.shape[0], A.stride(0), po, out.stride(0),
+                              _stream_ptr(stream)), "mdn_amm_probe")
     return out
 
 

@@ -209,7 +209,11 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
   }
 }
 
-template <class TIn, int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF>
+// PROBE (mdn_amm_probe): the same kernel -- producer, TMA boxes, stage and code
+// rings, barriers, grid, warp roles, output stores -- with Algorithm 1 and the
+// table scan removed (encoders only hand the stages back, scanners store
+// beta32 for every output): the data-movement ceiling of this pipeline.
+template <class TIn, int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF, bool PROBE = false>
 __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
     k_amm_ws(const __grid_constant__ CUtensorMap tmap, const Params p) {
   constexpr int G = C >= 8 ? 8 : C;      // codebooks per encoder unit (one code word)
@@ -333,7 +337,7 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
         const int s = q % p.NS;
         mbar_wait(&full[s], (q / p.NS) & 1u);
         const TIn* stg = s_stage + (size_t)s * stage_e;
-        for (int u = etid; u < p.R * NG; u += EW * 32) {
+        for (int u = etid; u < (PROBE ? 0 : p.R * NG); u += EW * 32) {
           // Group-fastest units: the lanes of a warp cover NG codebook groups of
           // 32 / NG rows, so their split columns differ and the per-row reads
           // (pitch == 4 mod 32 words) spread over more banks than 32 rows of
@@ -376,7 +380,12 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
         const int64_t row = tile * BR + rl;
         const uint32_t* myc = s_codes + (b * BR + rl) * CBW;
         uint32_t ae[W], ao[W];
-        scan_core<C, W, U, false, (SUBF == CM && W >= 8) ? MDN_CM_MIX : 0>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
+        if constexpr (PROBE) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) ae[w] = 0u, ao[w] = 0u;
+        } else {
+          scan_core<C, W, U, false, (SUBF == CM && W >= 8) ? MDN_CM_MIX : 0>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
+        }
         if (k == KR - 1) mbar_arrive(&cempty[b]);
         if (row < p.N)
           store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32, p.pair);
@@ -566,9 +575,9 @@ bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <class TIn, int C, int W, int U, bool VEC, bool ENC, int SUBF>
+template <class TIn, int C, int W, int U, bool VEC, bool ENC, int SUBF, bool PROBE = false>
 cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
-  auto k = k_amm_ws<TIn, C, W, U, VEC, ENC, SUBF>;
+  auto k = k_amm_ws<TIn, C, W, U, VEC, ENC, SUBF, PROBE>;
   cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (attr_err != cudaSuccess) return attr_err;
   int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
@@ -728,6 +737,39 @@ static cudaError_t amm_fast(const TreesDev& t, const LutsDev& l, const TIn* A, i
 #undef X
   *done = false;
   return cudaSuccess;
+}
+
+// mdn_amm_probe: amm_fast's geometry and launch with PROBE (row-major fp32 A).
+static cudaError_t amm_probe_fast(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
+                                  int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done) {
+  *done = false;
+  Geometry g;
+  if (N > (int64_t)0x7FFFFF00 || !amm_fast_ok(t, l, A, lda, 4, &g)) return cudaSuccess;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R, 4)) return cudaSuccess;
+  Params p = base_params(t, g, N);
+  p.ldo = ldo;
+  p.M = l.M;
+  p.pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
+  p.alpha_eff = l.alpha_eff;
+  p.beta32 = l.beta32;
+  p.lut = l.words;
+  p.out = out;
+  const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
+  *done = true;
+#define X(c, w, u)                                                                             \
+  if (u == 0 && t.C == c && l.W == w)                                                          \
+    return vec ? launch_ws_sf<float, c, w, 0, true, false, 0, true>(tm, p, g.smem, s)          \
+               : launch_ws_sf<float, c, w, 0, false, false, 0, true>(tm, p, g.smem, s);
+  MDN_FAST_COMBOS(X)
+#undef X
+  *done = false;
+  return cudaSuccess;
+}
+
+cudaError_t launch_amm_probe(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
+                             int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done) {
+  return amm_probe_fast(t, l, A, N, lda, out, ldo, s, done);
 }
 
 template <class TIn>

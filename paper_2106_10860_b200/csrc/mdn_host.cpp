@@ -16,6 +16,8 @@
 
 namespace mdn {
 
+cudaError_t launch_amm_probe(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
+                             int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done);
 cudaError_t launch_stream_probe(const float* A, int64_t N, int64_t lda, int D, float* out,
                                 int64_t ldo, int M, cudaStream_t s);
 
@@ -584,6 +586,28 @@ int mdn_amm(const mdn_model* m, const mdn_luts* l, const float* A, int64_t N, in
     return launch_amm(m->trees(), l->dev(), A + r0 * lda, n, lda, out + r0 * ldo, ldo,
                       (cudaStream_t)stream);
   }));
+}
+
+int mdn_amm_probe(const mdn_model* m, const mdn_luts* l, const float* A, int64_t N, int64_t lda,
+                  float* out, int64_t ldo, void* stream) {
+  if (!m || !l || N < 0) return MDN_EINVAL;
+  if (l->C != m->C) return MDN_ESHAPE;
+  if (l->model_fp != m->fingerprint || m->pq) return MDN_ESTATE;
+  if (l->device != m->device) return MDN_EINVAL;
+  if (N == 0) return MDN_OK;
+  if (!A || !out || lda < m->D || ldo < l->M) return MDN_EINVAL;
+  DeviceGuard g(m->device);
+  if (!g.ok) return MDN_ECUDA;
+  bool all_done = true;
+  int st = cuda_status(for_row_chunks(N, [&](int64_t r0, int64_t n) {
+    bool done = false;
+    cudaError_t e = launch_amm_probe(m->trees(), l->dev(), A + r0 * lda, n, lda, out + r0 * ldo,
+                                     ldo, (cudaStream_t)stream, &done);
+    all_done = all_done && done;
+    return e;
+  }));
+  if (st != MDN_OK) return st;
+  return all_done ? MDN_OK : MDN_EINVAL;   // no general (k_amm_ws) pipeline for this shape
 }
 
 int mdn_encode_u8(const mdn_model* m, const uint8_t* A, int64_t N, int64_t lda, uint8_t* codes,
