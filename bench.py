@@ -544,11 +544,13 @@ def run(args):
         dist.barrier()
     torch.cuda.synchronize()
     t_wall0 = time.time()
+    torch.cuda.nvtx.range_push(f"bench timed region rank {rank}")    # multi-GPU timeline
     ev[0].record(stream)
     for i in range(args.steps):
         step()
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     t_wall1 = time.time()
     if ws > 1:
         dist.barrier()

@@ -18,7 +18,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmaddness.so")
+# MDN_LIB: an in-tree variant build (build.py --variant NAME) for A/B experiments
+LIB_PATH = os.path.join(_PKG, os.environ.get("MDN_LIB", "libmaddness.so"))
 
 MDN_SUM_EXACT = 0
 MDN_SUM_AVG = 1

@@ -1,6 +1,9 @@
 """Build libmaddness.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-    python paper_2106_10860_b200/build.py [--force] [--verbose]
+    python paper_2106_10860_b200/build.py [--force] [--verbose] [--variant NAME]
+
+--variant NAME (A/B experiments only): objects in build/obj_NAME, library at
+paper_2106_10860_b200/libmaddness_NAME.so, loaded when MDN_LIB names it.
 
 Run it as a script (or via __graft_entry__.build()): `python -m` would first
 import the package, which loads -- and validates -- the current .so.
@@ -36,8 +39,8 @@ def _headers_mtime():
     return max(os.path.getmtime(h) for h in hs)
 
 
-def _compile(src, force, verbose):
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(src, force, verbose, build_dir=BUILD):
+    obj = os.path.join(build_dir, os.path.basename(src) + ".o")
     if (not force and os.path.exists(obj)
             and os.path.getmtime(obj) >= max(os.path.getmtime(src), _headers_mtime())):
         return obj, ""
@@ -48,28 +51,31 @@ def _compile(src, force, verbose):
     return obj, p.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    build_dir = BUILD + ("_" + variant if variant else "")
+    lib = LIB if not variant else os.path.join(PKG, f"libmaddness_{variant}.so")
+    os.makedirs(build_dir, exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        res = list(ex.map(lambda s: _compile(s, force, verbose), srcs))
+        res = list(ex.map(lambda s: _compile(s, force, verbose, build_dir), srcs))
     objs = [o for o, _ in res]
     if verbose:
         for _, log in res:
             if log:
                 sys.stderr.write(log)
-    if (force or not os.path.exists(LIB)
-            or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)):
-        tmp = LIB + ".tmp"
+    if (force or not os.path.exists(lib)
+            or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs)):
+        tmp = lib + ".tmp"
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + [
             "-lcuda", "-lcusolver", "-L/usr/local/cuda/lib64",
             "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stdout}\n{p.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, variant=var))

@@ -77,6 +77,9 @@ __host__ __device__ constexpr int off_base(int c) { return 4 * c + 4 * (c >> 3);
 #ifndef MDN_E_MID
 #define MDN_E_MID 6          // encoder warps for 3 <= W < 8 (tuning experiments: -DMDN_E_MID=...)
 #endif
+#ifndef MDN_S_MID
+#define MDN_S_MID 4          // scanner warps for 3 <= W < 8 (tuning experiments: -DMDN_S_MID=...)
+#endif
 
 template <int W, bool ENC_ONLY, bool CMV = false>
 struct Roles {
@@ -84,7 +87,7 @@ struct Roles {
   // (fewer bytes per row), so it gets 6 encoder warps instead of 2 (cls100:
   // 3.65 -> 4.11e9 rows/s; 2 encoder warps could not keep up).
   static constexpr int E = ENC_ONLY ? 8 : (W >= 8 ? (CMV ? MDN_CM_E : MDN_E_WIDE) : (W >= 3 ? MDN_E_MID : 8));
-  static constexpr int S = ENC_ONLY ? 0 : (W >= 8 ? 8 : (W >= 3 ? 4 : 2));
+  static constexpr int S = ENC_ONLY ? 0 : (W >= 8 ? 8 : (W >= 3 ? MDN_S_MID : 2));
   static constexpr int THREADS = 32 * (1 + E + S);
   static constexpr int ROWS_PER_SCANNER = ENC_ONLY ? 0 : BR / (32 * S);
 };
@@ -589,7 +592,9 @@ cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cu
 template <class TIn, int C, int W, int U, bool VEC, bool ENC>
 cudaError_t launch_ws_t(const CUtensorMap& tm, const Params& p, int subf, size_t smem,
                         cudaStream_t s) {
-  if constexpr (C <= 8) {
+  // and, for fp32 rows, the multi-slab uniform-subspace case of the scale
+  // config (C = 32 x 8 columns, W = 4 tables or encode-only)
+  if constexpr (C <= 8 || (sizeof(TIn) == 4 && (C == 16 || C == 32) && (W == 4 || ENC))) {
     if (subf == 1) return launch_ws_sf<TIn, C, W, U, VEC, ENC, 1>(tm, p, smem, s);
     if (subf == 2) return launch_ws_sf<TIn, C, W, U, VEC, ENC, 2>(tm, p, smem, s);
   }
@@ -658,7 +663,14 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 // es = input element size (4: fp32 A, 1: uint8 A).
 static int subf_for(const TreesDev& t, const Geometry& g, int es) {
-  if (g.nslab != 1) return 0;                 // subspace loads stay inside one slab
+  if (g.nslab != 1) {
+    // several slabs: subspace vector loads only where no subspace straddles a
+    // slab boundary (uniform 4- / 8-column subspaces, SW a multiple of the
+    // width; e.g. the scale config, 32 x 8 columns in two 128-column slabs)
+    static const bool wide = env_int("MDN_SUBF_SLABS", 1) != 0;   // A/B knob
+    if (es == 4 && wide && t.subf_uni > 0 && g.SW % (4 * t.subf_uni) == 0) return t.subf_uni;
+    return 0;
+  }
   return es == 4 ? t.subf : t.subf_u8;
 }
 
@@ -769,6 +781,8 @@ static cudaError_t amm_probe_fast(const TreesDev& t, const LutsDev& l, const flo
 
 cudaError_t launch_amm_probe(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
                              int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done) {
+  *done = false;
+  if (rt_enabled() && amm_rt_applies(t, l, 4)) return cudaSuccess;   // mdn_amm runs k_amm_rt here
   return amm_probe_fast(t, l, A, N, lda, out, ldo, s, done);
 }
 

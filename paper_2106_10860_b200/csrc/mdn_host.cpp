@@ -12,6 +12,8 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: no-ops unless a profiler attaches
+
 #include "mdn_internal.h"
 
 namespace mdn {
@@ -216,6 +218,12 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   }
   m->subf = aligned && max_w <= 4 ? 1 : (aligned && max_w <= 8 ? 2 : 0);
   // uint8 input: every subspace exactly 4 (or 8) bytes, back to back
+  m->subf_uni = 0;
+  for (int w : {4, 8}) {
+    bool ok = (int)D == w * (int)C;
+    for (uint32_t c = 0; c < C && ok; ++c) ok = m->h_sub[c] == w * c;
+    if (ok) m->subf_uni = w / 4;
+  }
   m->subf_u8 = 0;
   for (int w : {4, 8}) {
     bool ok = (int)D == w * (int)C;
@@ -786,6 +794,10 @@ int run_pipeline(mdn_exec* x, int64_t N, ChunkFn&& chunk) {
   // The staging slots are mutable state of the handle: one call at a time
   // (maddness.h: concurrent calls on one executor serialise here).
   std::lock_guard<std::mutex> lock(x->mu);
+  nvtxRangePushA("mdn_host_pipeline");          // timeline: one range per host call
+  struct PopRange {
+    ~PopRange() { nvtxRangePop(); }
+  } pop_range;
   DeviceGuard g(x->device);
   if (!g.ok) return MDN_ECUDA;
   cudaError_t e = cudaSuccess;
