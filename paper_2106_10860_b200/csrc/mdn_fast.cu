@@ -399,31 +399,91 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
 
 // ------------------------------------------------------------ scan kernel --
 
+// Code-word software pipelining of mdn_scan (the next row's code words are
+// loaded before this row is scanned): 0 = off, 1 = on with the codebook-group
+// loop rolled (words picked by selects), 2 = on with it unrolled. Measured
+// (same box, rows/s, mode 2 / 1 / 0): scale (C 32, W 4) 3.56 / 3.17 / 3.27e10,
+// cls10_c32 3.75 / 3.28 / 3.49e10, cls10_c64 2.12 / 1.83 / 1.80e10; cls100
+// (W 25) 1: 4.78 vs 0: 5.06e9 (unrolled: 3.95e9, register pressure); C = 16
+// within 2%. MDN_SCAN_PF (build flag) forces one mode for A/B.
+template <int C, int W>
+constexpr int scan_pf_mode() {
+#ifdef MDN_SCAN_PF
+  return MDN_SCAN_PF;
+#else
+  return C >= 32 && W <= 4 ? 2 : 0;
+#endif
+}
+
+// The row's packed code words (8 codes each); `vec`: rows 16-B (C = 32) or
+// 8-B (C = 16) aligned, one vector load.
+template <int C>
+__device__ __forceinline__ void load_code_words(const uint8_t* __restrict__ codes, int64_t row,
+                                                uint32_t (&cw)[C >= 8 ? C / 8 : 1], bool vec) {
+  const uint8_t* cr = codes + row * ((C + 1) / 2);
+  if constexpr (C == 32) {
+    if (vec) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(cr));
+      cw[0] = v.x, cw[1] = v.y, cw[2] = v.z, cw[3] = v.w;
+      return;
+    }
+  } else if constexpr (C == 16) {
+    if (vec) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(cr));
+      cw[0] = v.x, cw[1] = v.y;
+      return;
+    }
+  }
+  if constexpr (C >= 8) {
+#pragma unroll
+    for (int g = 0; g < C / 8; ++g) cw[g] = __ldg(reinterpret_cast<const uint32_t*>(cr) + g);
+  } else if constexpr (C == 4) {
+    cw[0] = __ldg(reinterpret_cast<const uint16_t*>(cr));
+  } else {
+    cw[0] = __ldg(cr);
+  }
+}
+
 template <int C, int W, int U, bool VEC, int MIX>
 __global__ void __launch_bounds__(256) k_scan_fast(const uint32_t* __restrict__ lut_g,
                                                    const uint8_t* __restrict__ codes, int64_t N,
                                                    int M, int32_t* __restrict__ sums,
                                                    float* __restrict__ out, int64_t ldo, float a,
-                                                   float b, int scale, bool pair) {
+                                                   float b, int scale, bool pair, bool vec_codes) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
   for (int i = threadIdx.x; i < C * W * 4; i += blockDim.x)
     reinterpret_cast<uint4*>(s_lut)[i] = reinterpret_cast<const uint4*>(lut_g)[i];
   __syncthreads();
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < N;
-       row += (int64_t)gridDim.x * blockDim.x) {
-    const uint8_t* cr = codes + row * ((C + 1) / 2);
+  constexpr int NW = C >= 8 ? C / 8 : 1;
+  constexpr int PF = scan_pf_mode<C, W>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t cw[NW];
+  if (PF && row < N) load_code_words<C>(codes, row, cw, vec_codes);
+  for (; row < N; row += stride) {
+    uint32_t nx[NW];
+    if constexpr (PF != 0) {
+      if (row + stride < N) load_code_words<C>(codes, row + stride, nx, vec_codes);
+    } else {
+      load_code_words<C>(codes, row, cw, vec_codes);
+    }
     uint32_t ae[W], ao[W];
-    scan_core<C, W, U, false, MIX>(
+    scan_core<C, W, U, PF == 2, MIX>(
         s_lut,
-        [&](int g) -> uint32_t {
-          if constexpr (C >= 8) return __ldg(reinterpret_cast<const uint32_t*>(cr) + g);
-          else if constexpr (C == 4) return __ldg(reinterpret_cast<const uint16_t*>(cr));
-          else return __ldg(cr);
+        [&](int g) {
+          uint32_t r = cw[0];
+#pragma unroll
+          for (int k = 1; k < NW; ++k) r = g == k ? cw[k] : r;   // register select, no local memory
+          return r;
         },
         ae, ao);
     if (sums) store_sums<W>(sums + row * M, M, scale, ae, ao);
     if (out) store_row<W, VEC>(out + row * ldo, M, ae, ao, a, b, pair);
+    if constexpr (PF != 0) {
+#pragma unroll
+      for (int g = 0; g < NW; ++g) cw[g] = nx[g];
+    }
   }
 }
 
@@ -592,9 +652,7 @@ cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cu
 template <class TIn, int C, int W, int U, bool VEC, bool ENC>
 cudaError_t launch_ws_t(const CUtensorMap& tm, const Params& p, int subf, size_t smem,
                         cudaStream_t s) {
-  // and, for fp32 rows, the multi-slab uniform-subspace case of the scale
-  // config (C = 32 x 8 columns, W = 4 tables or encode-only)
-  if constexpr (C <= 8 || (sizeof(TIn) == 4 && (C == 16 || C == 32) && (W == 4 || ENC))) {
+  if constexpr (C <= 8) {
     if (subf == 1) return launch_ws_sf<TIn, C, W, U, VEC, ENC, 1>(tm, p, smem, s);
     if (subf == 2) return launch_ws_sf<TIn, C, W, U, VEC, ENC, 2>(tm, p, smem, s);
   }
@@ -632,8 +690,9 @@ cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int
   const int64_t cap = (int64_t)dev_info().sms * per_sm;
   if (blocks > cap) blocks = cap;
   const bool pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
+  const bool vec_codes = (reinterpret_cast<uintptr_t>(codes) & (C == 32 ? 15u : 7u)) == 0;
   k<<<(unsigned)blocks, 256, smem, s>>>(l.words, codes, N, l.M, sums, out, ldo, l.alpha_eff,
-                                        l.beta32, l.U == 0 ? 1 : l.U, pair);
+                                        l.beta32, l.U == 0 ? 1 : l.U, pair, vec_codes);
   return cudaGetLastError();
 }
 
@@ -663,14 +722,11 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 // es = input element size (4: fp32 A, 1: uint8 A).
 static int subf_for(const TreesDev& t, const Geometry& g, int es) {
-  if (g.nslab != 1) {
-    // several slabs: subspace vector loads only where no subspace straddles a
-    // slab boundary (uniform 4- / 8-column subspaces, SW a multiple of the
-    // width; e.g. the scale config, 32 x 8 columns in two 128-column slabs)
-    static const bool wide = env_int("MDN_SUBF_SLABS", 1) != 0;   // A/B knob
-    if (es == 4 && wide && t.subf_uni > 0 && g.SW % (4 * t.subf_uni) == 0) return t.subf_uni;
-    return 0;
-  }
+  // Subspace loads stay inside one slab. (Allowing them across the two
+  // 128-column slabs of the scale config -- 32 uniform 8-column subspaces --
+  // cost 21%: 4.62 vs 5.86e9 rows/s, same box; the groups' 16-B loads land
+  // on the same banks.)
+  if (g.nslab != 1) return 0;
   return es == 4 ? t.subf : t.subf_u8;
 }
 

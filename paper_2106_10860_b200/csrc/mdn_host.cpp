@@ -218,12 +218,6 @@ int mdn_model_load(const void* buf, size_t len, int device, mdn_model** out, siz
   }
   m->subf = aligned && max_w <= 4 ? 1 : (aligned && max_w <= 8 ? 2 : 0);
   // uint8 input: every subspace exactly 4 (or 8) bytes, back to back
-  m->subf_uni = 0;
-  for (int w : {4, 8}) {
-    bool ok = (int)D == w * (int)C;
-    for (uint32_t c = 0; c < C && ok; ++c) ok = m->h_sub[c] == w * c;
-    if (ok) m->subf_uni = w / 4;
-  }
   m->subf_u8 = 0;
   for (int w : {4, 8}) {
     bool ok = (int)D == w * (int)C;

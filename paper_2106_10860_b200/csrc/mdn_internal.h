@@ -33,8 +33,6 @@ struct TreesDev {
   int D;
   int subf;              // fp32: 1 / 2 = every subspace 16-B aligned and <= 4 / 8 wide
   int subf_u8;           // uint8: 1 / 2 = every subspace exactly 4 / 8 bytes, contiguous
-  int subf_uni;          // fp32: 1 / 2 = every subspace exactly 4 / 8 columns at a multiple
-                         // of its width (never straddles a slab of SW % (4 subf) == 0)
   int q_byte;            // every 8-bit split value q <= 255 (fits a byte)
   const uint16_t* cols;  // distinct split columns, ascending [n_cols] (column-major A)
   const uint16_t* slot;  // [D] index of each split column in `cols` (0xFFFF otherwise)
@@ -129,7 +127,7 @@ struct mdn_model {
   std::vector<float> h_thr;       // [C][16]
   std::vector<uint16_t> h_sub;    // [C] subspace begin
   std::vector<uint16_t> h_q;      // [C][16] 8-bit split values
-  int subf = 0, subf_u8 = 0, subf_uni = 0, q_byte = 0;
+  int subf = 0, subf_u8 = 0, q_byte = 0;
   std::vector<uint16_t> h_cols, h_slot;
   uint16_t* d_cols = nullptr;
   uint16_t* d_slot = nullptr;
@@ -144,7 +142,7 @@ struct mdn_model {
   uint16_t* d_q = nullptr;
   float* d_P = nullptr;           // [16C][D]
   mdn::TreesDev trees() const {
-    return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8, subf_uni, q_byte, d_cols, d_slot,
+    return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8, q_byte, d_cols, d_slot,
             (int)h_cols.size(), d_pqcent, d_pqcent ? pq_ds : 0};
   }
 };

@@ -63,9 +63,18 @@ def full(rep, out, key=None):
     with open(out, "w") as f:
         json.dump({"report": os.path.basename(rep), "launches": launches}, f, indent=1)
     if key and launches:
+        # profiles/traffic.json: {"_meta": {csrc hash the captures ran on, source},
+        # "values": {key: DRAM bytes per launch}}; bench.py flags a figure whose
+        # hash differs from the current sources as stale.
+        sys.path.insert(0, ROOT)
+        from bench import csrc_sha256
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         t = json.load(open(tp)) if os.path.exists(tp) else {}
-        t[key] = launches[0]["traffic_bytes"]
+        if "values" not in t or t.get("_meta", {}).get("csrc_sha256") != csrc_sha256():
+            t = {"values": {}}              # captures of other sources are not mixed in
+        t["_meta"] = {"csrc_sha256": csrc_sha256(),
+                      "source": os.environ.get("NCU_SOURCE", "profiles/r02/ncu_full_*.json")}
+        t["values"][key] = launches[0]["traffic_bytes"]
         json.dump(t, open(tp, "w"), indent=1, sort_keys=True)
     for rec in launches:
         print(json.dumps(rec, indent=1))
