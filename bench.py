@@ -813,8 +813,15 @@ def run(args):
                        "3-slot pipelined H2D/kernel/D2H)"}
         ex.close()
         del At_h, out_h
+    if e2e is not None:
+        # what bounds the host-buffer path: the PCIe host->device stream of the
+        # step's inputs (~52-54 GB/s measured on this pool's hosts), not the kernel
+        t_step = e2e["rows_per_step"] / e2e["value"]
+        e2e["h2d_gbs_achieved"] = e2e["h2d_bytes_per_step"] / t_step / 1e9
+        e2e["bound"] = "PCIe host->device copy of the step's inputs"
 
-    # --- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1 only ---
+    # --- CPU baseline: the oracle on a bounded sample (rank 0; at N > 1 after
+    # every rank's timed region) ---
     cpu = None
     # (at N > 1 rank 0 runs it after every rank's timed region; the others wait)
     if rank == 0 and not args.no_cpu_baseline and op == "amm" and not col and not pq:
