@@ -21,4 +21,16 @@ bash scripts/ncu_capture.sh \
   image_u8_encode_exact k_amm_rt --config image_u8 --op encode -- \
   cls100_scan_exact k_scan_fast --config cls100 --op scan -- \
   image_scan_exact k_scan_fast --config image --op scan -- \
-  cls100_encode_pq_exact k_encode_pq --config cls100 --op encode --encoder pq
+  cls100_encode_pq_exact k_encode_pq --config cls100 --op encode --encoder pq -- \
+  scale_encode_pq_exact k_encode_pq --config scale --op encode --encoder pq -- \
+  cls10_c16_encode_pq_exact k_encode_pq --config cls10_c16 --op encode --encoder pq -- \
+  scale_scan_exact k_scan_fast --config scale --op scan -- \
+  cls100_scan_avg k_scan_fast --config cls100 --op scan --mode avg
+# the pipeline probe (mdn_amm_probe) of the headline config: same kernel name
+# as the fused kernel, told apart by its template arguments
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k 'regex:k_amm_ws<float, 32, 25, 0, true, false, 0, true>' -c 1 -f \
+    -o ${NCU_OUT:-gpurun_out}/prof_cls100_probe \
+    python bench.py --config cls100 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_cls100_probe.log 2>&1
+[ -n "$NCU_SUMMARY" ] && python scripts/ncu_summary.py full ${NCU_OUT:-gpurun_out}/prof_cls100_probe.ncu-rep \
+    gpurun_out/ncu_full_cls100_probe.json > /dev/null 2>&1
