@@ -48,3 +48,23 @@ def test_traffic_lookup_tags_source_hash(tmp_path, monkeypatch):
     v, src = bench.traffic_lookup("k_exact")
     assert v == 5.0 and src["stale"]
     assert bench.traffic_lookup("missing") == (None, None)
+
+
+def test_reference_arm_rank_contract():
+    """--impl reference under a 2-rank launch: rank 1 exits 0 without output;
+    rank 0 prints one line with the oracle's rate and the reference keys."""
+    base = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+            "--steps", "2", "--warmup", "3"]
+    env1 = dict(os.environ, WORLD_SIZE="2", RANK="1", LOCAL_RANK="1")
+    p = subprocess.run(base, env=env1, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0 and p.stdout.strip() == ""
+    env0 = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run(base, env=env0, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "rows/s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["steps"] == 2 and d["warmup"] == 3
