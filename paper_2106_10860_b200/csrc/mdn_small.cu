@@ -66,7 +66,14 @@ template <class TIn, bool ENC> constexpr int subs_of() {
 }
 template <class TIn, bool ENC> constexpr int cps_of() { return R / (32 * subs_of<TIn, ENC>()); }
 template <class TIn, bool ENC> constexpr int ng_of() { return NWK / cps_of<TIn, ENC>(); }
-constexpr int NS_MAX = 8;
+#ifndef MDN_RT_NS_MAX
+#define MDN_RT_NS_MAX 16
+#endif
+// Stage ring depth cap. 8-bit stages are 8 KB (256 rows x 32 B): 8 stages keep
+// only 64 KB per SM in flight, under the bytes HBM latency needs at 35 GB/s
+// per SM; 16 (the barrier block's 256 bytes hold 2 x 16) lift that to 128 KB.
+constexpr int NS_MAX = MDN_RT_NS_MAX;
+static_assert(2 * NS_MAX * 8 <= 256, "full/empty barriers must fit below OFF_LUT");
 #ifndef MDN_RT_CTAS_U8
 #define MDN_RT_CTAS_U8 1     // resident CTAs per SM of the 8-bit variants (tuning: -DMDN_RT_CTAS_U8=2)
 #endif
@@ -250,7 +257,8 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
   __syncthreads();
 
   // Local stage sequence of this CTA: tiles blockIdx.x, blockIdx.x + grid, ...
-  const int64_t n_local = (p.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  // stages of this CTA (< 2^31: N < 2^31 rows are checked on the host)
+  const int n_local = (int)((p.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -258,7 +266,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
       const uint32_t bytes = (uint32_t)(R * p.pitch_e * sizeof(TIn));
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t q = 0; q < n_local; ++q) {
+      for (int q = 0; q < n_local; ++q) {
         mbar_wait_sleep(&empty[s], ph ^ 1u);
         mbar_arrive_tx(&full[s], bytes);
         const int64_t y = (blockIdx.x + q * gridDim.x) * (int64_t)R;
@@ -338,11 +346,15 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
   int s = grp, ph = 0;
   while (s >= p.NS) s -= p.NS, ph ^= 1;
   // This lane's output row and pointer, advanced by a constant stride per stage.
-  int64_t row = ((int64_t)blockIdx.x + (int64_t)grp * gridDim.x) * R + chunk * 32 * SUBS + lane;
-  const int64_t row_step = (int64_t)NG * gridDim.x * R;
-  float* o_row = p.out + row * p.ldo;
-  const int64_t o_step = row_step * p.ldo;
-  for (int64_t q = grp; q < n_local; q += NG, row += row_step, o_row += o_step) {
+  // 32-bit row counter: N <= 0x7FFFFF00 (host check), unsigned wrap past the
+  // last stage is never compared
+  uint32_t row = ((uint32_t)blockIdx.x + (uint32_t)grp * gridDim.x) * R + chunk * 32 * SUBS + lane;
+  const uint32_t row_step = (uint32_t)NG * gridDim.x * R;
+  const uint32_t n_rows = (uint32_t)p.N;
+  float* o_row = p.out + (int64_t)row * p.ldo;
+  const int64_t o_step = (int64_t)row_step * p.ldo;
+  const float alpha = p.alpha_eff, beta = p.beta32;
+  for (int q = grp; q < n_local; q += NG, row += row_step, o_row += o_step) {
     mbar_wait_sleep(&full[s], (uint32_t)ph);
 #pragma unroll 1
     for (int hs = 0; hs < SUBS; ++hs) {
@@ -394,7 +406,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
         const uint32_t r = __shfl_xor_sync(0xffffffffu, t, 1 << k);
         keep = (keep & t_sel[k]) | (r & ~t_sel[k]);
       }
-      const int64_t r = ((int64_t)blockIdx.x + q * gridDim.x) * R + chunk * 32 * SUBS + hs * 32 +
+      const int64_t r = ((int64_t)blockIdx.x + (int64_t)q * gridDim.x) * R + chunk * 32 * SUBS + hs * 32 +
                         c * RPW + rs;
       if (r < p.N) {
         if constexpr (C == 8)
@@ -449,13 +461,13 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
           acc[w] += v[0];
         }
     }
-    if (row + hs * 32 < p.N) {
+    if (row + hs * 32 < n_rows) {
       float* o_h = o_row + (int64_t)hs * 32 * p.ldo;
       float f[2 * W2];
 #pragma unroll
       for (int w = 0; w < W2; ++w) {
-        f[2 * w] = __fmaf_rn(p.alpha_eff, u16_to_f(acc[w] & 0xFFFFu), p.beta32);
-        f[2 * w + 1] = __fmaf_rn(p.alpha_eff, u16_to_f(acc[w] >> 16), p.beta32);
+        f[2 * w] = __fmaf_rn(alpha, u16_to_f(acc[w] & 0xFFFFu), beta);
+        f[2 * w + 1] = __fmaf_rn(alpha, u16_to_f(acc[w] >> 16), beta);
       }
       if constexpr (VEC) {
         if constexpr (W2 % 2 == 0) {
@@ -474,8 +486,9 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
       }
     }
     }  // chunks of the stage
+    // next ring slot of this group: NS % NG == 0 and NG <= NS, so one wrap at most
     s += NG;
-    while (s >= p.NS) s -= p.NS, ph ^= 1;
+    if (s >= p.NS) s -= p.NS, ph ^= 1;
   }
 }
 
