@@ -34,6 +34,11 @@ constexpr int THREADS = 256;
 // (more registers, fewer resident warps) on every config; off
 #define MDN_PQ_PF 0
 #endif
+// Also measured and rejected: packed fp32x2 FMAs (FFMA2, row pairs, the
+// prototype value as the broadcast scalar operand -- half the FMA
+// instructions) ran at 0.75 of the scalar-FFMA kernel (cls100 1.32 vs 1.76e9,
+// scale 2.36 vs 3.11e9, tiny 1.87 vs 2.50e10 rows/s): FFMA2 does not double
+// the fp32 rate and halves the independent accumulator chains.
 #ifndef MDN_PQ_R4
 #define MDN_PQ_R4 8     // rows per thread for 4-column subspaces
 #endif
