@@ -51,6 +51,17 @@ namespace fast {
 namespace small {
 
 constexpr int R = 256;                   // rows per stage (= TMA box rows)
+#ifndef MDN_RT_LANE_LUT
+#define MDN_RT_LANE_LUT 1
+#endif
+// Scan tables replicated per scanner lane: word (c, k, w) of lane l at
+// ((c 16 + k) W2 + w) 32 + l, so lane l's lookups always hit bank l -- any
+// code mix is conflict-free (one shared copy of 16 words per codebook put the
+// 32 rows' random codes on 16 banks: ~38% of the kernel's shared-load
+// wavefronts were conflicts). 16 KB for W2 = 1. On for 8-bit rows (image_u8
+// 1.341 -> 1.366e11 rows/s, same box); fp32 rows are HBM-bound and their
+// W2 = 2 tables (32 KB) cost the tiny config a stage (-0.8%), so not there.
+template <class TIn> constexpr int lanes_lut() { return sizeof(TIn) == 1 && MDN_RT_LANE_LUT ? 32 : 1; }
 constexpr int NWK = 16;                  // worker warps
 constexpr int THREADS = 32 * (1 + NWK);
 #ifndef MDN_RT_SUBS_U8_ENC
@@ -196,7 +207,7 @@ __device__ __forceinline__ uint32_t byte_tree_n4(uint32_t w, const ByteTree& b) 
 
 template <int W2>
 __device__ __forceinline__ uint32_t byte_tree_addr(uint32_t w, const ByteTree& b) {
-  return b.base - byte_tree_n4(w, b) * (4u * W2);   // 15 - n4 = code
+  return b.base - byte_tree_n4(w, b) * (4u * W2 * lanes_lut<uint8_t>());   // 15 - n4 = code
 }
 
 // mu(a, b) = floor((a + b + 1) / 2) on two 16-bit lanes holding values < 256
@@ -238,14 +249,16 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NS_MAX;
   constexpr int OFF_LUT = 256;
-  constexpr int OFF_CODE = OFF_LUT + C * 16 * W2 * 4;
+  constexpr int LANES_LUT = lanes_lut<TIn>();
+  constexpr bool LANE_LUT = LANES_LUT > 1;
+  constexpr int OFF_CODE = OFF_LUT + C * 16 * W2 * 4 * LANES_LUT;
   constexpr int OFF_STAGE = ENC ? 256 : (OFF_CODE + NWK * 32 * CS * 4 + 127) & ~127;
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
 
   if constexpr (!ENC)
-    for (int i = tid; i < C * 16 * W2; i += blockDim.x) s_lut[i] = p.lut16[i];
+    for (int i = tid; i < C * 16 * W2 * LANES_LUT; i += blockDim.x) s_lut[i] = p.lut16[i / LANES_LUT];
   if (tid == 0) {
     for (int s = 0; s < p.NS; ++s) {
       mbar_init(&full[s], 1);
@@ -304,7 +317,10 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
   // Per-lane addressing, fixed for the kernel: the lane reads row rs of each
   // RPW-row group; the codebook's table base (absolute shared address) is
   // folded into the stored code so the scanner's lookups need no adds.
-  const uint32_t lut_c = su32(s_lut) + (uint32_t)(c * 16 * W2 * 4);
+  // (with per-lane tables: + 4 rs, the scanner lane of this lane's row in each
+  // RPW-row group; the group's 4 RPW it is added per iteration)
+  const uint32_t lut_c = su32(s_lut) + (uint32_t)(c * 16 * W2 * 4 * LANES_LUT) +
+                         (LANE_LUT ? 4u * (uint32_t)rs : 0u);
   ByteTree bt{};
   if constexpr (BQ) {
     const uint16_t* qc = p.q + c * 16;             // heap order; complemented node n at level t
@@ -329,7 +345,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
     bt.nd12s = 0u - ((uint32_t)bt.d12 << 16);
     bt.s2 = j2 | 0x4440u;                          // (x, g, g, g)
     bt.s3 = j3 | 0x4440u;
-    bt.base = lut_c + 15u * 4u * W2;
+    bt.base = lut_c + 15u * 4u * W2 * LANES_LUT;
   }
   // ENC transpose constants: stage k exchanges with lane c ^ 2^k; a lane whose
   // bit k is b keeps the nibbles whose index has bit k == b and receives the
@@ -374,9 +390,9 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
         if constexpr (BQ && ENC)
           code[it] = 15u - byte_tree_n4(w[it], bt);
         else if constexpr (BQ)
-          code[it] = byte_tree_addr<W2>(w[it], bt);
+          code[it] = byte_tree_addr<W2>(w[it], bt) + (LANE_LUT ? 4u * RPW * it : 0u);
         else
-          code[it] = (ENC ? 0u : lut_c) + (ENC ? 1u : 4u * W2) *
+          code[it] = (ENC ? 0u : lut_c + (LANE_LUT ? 4u * RPW * it : 0u)) + (ENC ? 1u : 4u * W2 * LANES_LUT) *
                      tree_code<int>((int)__byte_perm(w[it], 0u, sel[0]), (int)__byte_perm(w[it], 0u, sel[1]),
                                     (int)__byte_perm(w[it], 0u, sel[2]), (int)__byte_perm(w[it], 0u, sel[3]), th);
       }
@@ -388,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
         for (int t = 0; t < 4; ++t) x[it][t] = stg[it * RPW * PITCH + o[t]];
 #pragma unroll
       for (int it = 0; it < C; ++it)
-        code[it] = (ENC ? 0u : lut_c) + (ENC ? 1u : 4u * W2) *
+        code[it] = (ENC ? 0u : lut_c + (LANE_LUT ? 4u * RPW * it : 0u)) + (ENC ? 1u : 4u * W2 * LANES_LUT) *
                    tree_code<float>(x[it][0], x[it][1], x[it][2], x[it][3], th);
     }
     if constexpr (ENC) {
@@ -441,7 +457,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
       for (int cc = 0; cc < C; ++cc)
 #pragma unroll
         for (int w = 0; w < W2; ++w)
-          acc[w] += lds_u32(off[cc] + 4 * w);
+          acc[w] += lds_u32(off[cc] + 4 * LANES_LUT * w);
     } else {
       static_assert((U & (U - 1)) == 0 && C % U == 0, "U must be a power of two dividing C");
 #pragma unroll
@@ -452,7 +468,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
 #pragma unroll
           for (int i = 0; i < U; ++i) {
             const int cc = blk * U + i;
-            v[i] = lds_u32(off[cc] + 4 * w);
+            v[i] = lds_u32(off[cc] + 4 * LANES_LUT * w);
           }
 #pragma unroll
           for (int st = 1; st < U; st *= 2)          // halves recursion = adjacent pairs (R17)
@@ -553,7 +569,7 @@ static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int
   const int pitch_e = es == 1 ? t.D : t.D + 16 / es;     // must match the kernel's PITCH
   const int stage_b = ((R * pitch_e * es) + 127) & ~127;
   const int W2 = (l.M + 1) / 2;
-  const size_t fixed = ((256 + (size_t)t.C * 16 * W2 * 4 + (size_t)NWK * 32 * (t.C == 8 ? 12 : 4) * 4) + 127) & ~size_t(127);
+  const size_t fixed = ((256 + (size_t)t.C * 16 * W2 * 4 * lanes_lut<TIn>() + (size_t)NWK * 32 * (t.C == 8 ? 12 : 4) * 4) + 127) & ~size_t(127);
   size_t budget = (size_t)dev_info().smem_optin;
   if (es == 1 && MDN_RT_CTAS_U8 > 1) budget = std::min(budget, (size_t)(233472 / MDN_RT_CTAS_U8 - 1024));
   constexpr int NG = ng_of<TIn, false>();
