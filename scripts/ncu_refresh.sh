@@ -29,7 +29,7 @@ bash scripts/ncu_capture.sh \
 # the pipeline probe (mdn_amm_probe) of the headline config: same kernel name
 # as the fused kernel, told apart by its template arguments
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:k_amm_ws<float, 32, 25, 0, true, false, 0, true>' -c 1 -f \
+    -k 'regex:k_amm_ws<float, \(int\)32, \(int\)25, \(int\)0, \(bool\)1, \(bool\)0, \(int\)0, \(bool\)1>' -c 1 -f \
     -o ${NCU_OUT:-gpurun_out}/prof_cls100_probe \
     python bench.py --config cls100 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_cls100_probe.log 2>&1
 [ -n "$NCU_SUMMARY" ] && python scripts/ncu_summary.py full ${NCU_OUT:-gpurun_out}/prof_cls100_probe.ncu-rep \
