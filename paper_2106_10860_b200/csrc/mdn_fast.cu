@@ -41,10 +41,7 @@ namespace mdn {
 namespace fast {
 
 constexpr int BR = 256;                  // rows per tile
-#ifndef MDN_NB
-#define MDN_NB 3
-#endif
-constexpr int NB = MDN_NB;               // code ring depth (tiles)
+constexpr int NB = 3;                    // code ring depth (tiles)
 constexpr int NS_MAX = 8;                // A stage ring depth cap
 constexpr int BAR_BYTES = 256;
 constexpr int CM = -1;                   // SUBF value of the column-major-A variant
