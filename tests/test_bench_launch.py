@@ -68,3 +68,34 @@ def test_reference_arm_rank_contract():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["steps"] == 2 and d["warmup"] == 3
+
+
+def test_rank_parity_leg_detects_a_wrong_row():
+    """The bench's untimed parity leg: on outputs that equal the oracle's it
+    reports ok; one flipped output bit in a sampled row (the shard's last rows
+    are always sampled) is reported as one mismatched row; a wrong code the
+    same way for the encode op."""
+    import numpy as np
+    import torch
+    import oracle as O
+    from datagen.synth import make_config_data
+    from helpers import model_bytes
+    blob = model_bytes("tiny")
+    om = O.read_model(blob)
+    _, A, B = make_config_data("tiny", n_test=2048)
+    ol = O.make_luts(om, B, "exact", 4)
+    codes, _, out = O.amm(A, om, ol)
+    tA, tout = torch.from_numpy(A), torch.from_numpy(out.copy())
+    tcodes = torch.from_numpy(O.pack_codes(codes))
+    r = bench.rank_parity(tA, tout, tcodes, blob, B, "tiny", "exact", "amm", False, False, 0, 512)
+    assert r["ok"] and r["mismatched_rows"] == 0 and r["rows"] >= 512
+    bad = out.copy()
+    bad.view(np.uint32)[-1, 0] ^= 1                       # last row: always sampled
+    r = bench.rank_parity(tA, torch.from_numpy(bad), tcodes, blob, B, "tiny", "exact", "amm",
+                          False, False, 0, 512)
+    assert not r["ok"] and r["mismatched_rows"] == 1
+    bc = O.pack_codes(codes)
+    bc[-2, 0] ^= 0x10
+    r = bench.rank_parity(tA, tout, torch.from_numpy(bc), blob, B, "tiny", "exact", "encode",
+                          False, False, 0, 512)
+    assert not r["ok"] and r["mismatched_rows"] == 1
