@@ -124,7 +124,7 @@ class Model:
         self.C, self.D, self.fingerprint = C.value, D.value, fp.value
 
     def close(self):
-        if self._h:
+        if self._h and _lib is not None:      # _lib is None during interpreter teardown
             _lib.mdn_model_free(self._h)
             self._h = None
 
@@ -145,7 +145,7 @@ class Luts:
         self.alpha, self.beta32, self.model_fingerprint = np.float32(a.value), np.float32(b.value), fp.value
 
     def close(self):
-        if self._h:
+        if self._h and _lib is not None:
             _lib.mdn_luts_free(self._h)
             self._h = None
 
@@ -159,7 +159,7 @@ class Exec:
         self._h, self._model, self._luts = handle, model, luts
 
     def close(self):
-        if self._h:
+        if self._h and _lib is not None:
             _lib.mdn_exec_free(self._h)
             self._h = None
 

@@ -100,6 +100,8 @@ struct Params {
   int slab_e;                     // shared-memory elements (of the input type) per slab, 128-B aligned
   int pad_e;                      // row pitch = SW + pad_e elements (16 bytes of padding)
   int M;
+  int ntile;                      // TILED: column tiles of W words (ceil(Wfull / W))
+  int Wfull;                      // TILED: the tables' full width in words (ceil(M / 4))
   bool pair;                      // M even, ldo even, out 8-B aligned: 8-byte stores
   int l2_hint;                    // 0 none (default), 1 evict_first, 2 evict_last, 3 evict_normal
   float alpha_eff, beta32;
@@ -216,15 +218,23 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
 // rings, barriers, grid, warp roles, output stores -- with Algorithm 1 and the
 // table scan removed (encoders only hand the stages back, scanners store
 // beta32 for every output): the data-movement ceiling of this pipeline.
-template <class TIn, int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF, bool PROBE = false>
-__global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
+// TILED: table widths without a compiled kernel. The tables are cut into
+// p.ntile column tiles of W words (16 output columns for W = 4), laid out
+// [tile][c][W][16] after the stage ring, and every scanner row walks the
+// tiles: scan_core of tile t, then the row's columns [16 t, 16 t + 16). The
+// encoders and the code hand-off are unchanged; warp roles are the wide-table
+// ones (E2:S8 from W = 8), since a row then costs ntile times a W-word scan.
+template <class TIn, int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF, bool PROBE = false,
+          bool TILED = false>
+__global__ void __launch_bounds__(Roles<(TILED ? 8 : W), ENC_ONLY, SUBF == CM>::THREADS, 1)
     k_amm_ws(const __grid_constant__ CUtensorMap tmap, const Params p) {
   constexpr int G = C >= 8 ? 8 : C;      // codebooks per encoder unit (one code word)
   constexpr int NG = C / G;
   constexpr int CBW = NG;                // code words per row
-  constexpr int EW = Roles<W, ENC_ONLY, SUBF == CM>::E;
-  constexpr int SWN = Roles<W, ENC_ONLY, SUBF == CM>::S;
-  constexpr int KR = Roles<W, ENC_ONLY, SUBF == CM>::ROWS_PER_SCANNER;
+  constexpr int WR = TILED ? 8 : W;       // table width the warp roles are sized for
+  constexpr int EW = Roles<WR, ENC_ONLY, SUBF == CM>::E;
+  constexpr int SWN = Roles<WR, ENC_ONLY, SUBF == CM>::S;
+  constexpr int KR = Roles<WR, ENC_ONLY, SUBF == CM>::ROWS_PER_SCANNER;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + NS_MAX;
@@ -237,18 +247,20 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
   constexpr int OFF_BASE = OFF_OFF + off_base(C) * 4;
   constexpr int OFF_COLS = OFF_BASE + C * 4;
   constexpr int OFF_LUT = (OFF_COLS + (SUBF == CM ? 4 * C * 4 : 0) + 15) & ~15;
-  constexpr int OFF_CODES = OFF_LUT + (ENC_ONLY ? 0 : C * W * 16 * 4);
+  constexpr int OFF_CODES = OFF_LUT + (ENC_ONLY || TILED ? 0 : C * W * 16 * 4);
   constexpr int OFF_STAGE = (OFF_CODES + (ENC_ONLY ? 0 : NB * BR * CBW * 4) + 127) & ~127;
   float* s_thr = reinterpret_cast<float*>(smem + OFF_THR);
   int* s_off = reinterpret_cast<int*>(smem + OFF_OFF);
   int* s_base = reinterpret_cast<int*>(smem + OFF_BASE);
   int* s_cols = reinterpret_cast<int*>(smem + OFF_COLS);
-  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
   uint32_t* s_codes = reinterpret_cast<uint32_t*>(smem + OFF_CODES);
   TIn* s_stage = reinterpret_cast<TIn*>(smem + OFF_STAGE);
   const int tid = threadIdx.x;
   const int pitch = p.SW + p.pad_e;                 // elements of TIn per shared row
   const int stage_e = p.nslab * p.slab_e;
+  // tiled tables live after the stage ring (their size is a runtime value)
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(
+      smem + (TILED ? OFF_STAGE + (size_t)p.NS * stage_e * sizeof(TIn) : (size_t)OFF_LUT));
 
   // ---- setup: trees, split-dim offsets, tables, barriers ----
   for (int i = tid; i < 16 * C; i += blockDim.x) {
@@ -272,7 +284,15 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
     const int b = p.sub[c];
     s_base[c] = (b / p.SW) * p.slab_e + (b % p.SW);
   }
-  if constexpr (!ENC_ONLY) {
+  if constexpr (TILED) {
+    // [c][Wfull][16] -> [tile][c][W][16], words past the table width zero
+    const int n = p.ntile * C * W * 16;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const int k = i & 15, w = (i >> 4) % W, c = (i / (16 * W)) % C, t = i / (16 * W * C);
+      const int gw = t * W + w;
+      s_lut[i] = gw < p.Wfull ? p.lut[((size_t)c * p.Wfull + gw) * 16 + k] : 0u;
+    }
+  } else if constexpr (!ENC_ONLY) {
     const uint4* src = reinterpret_cast<const uint4*>(p.lut);
     uint4* dst = reinterpret_cast<uint4*>(s_lut);
     for (int i = tid; i < C * W * 4; i += blockDim.x) dst[i] = src[i];
@@ -383,6 +403,17 @@ __global__ void __launch_bounds__(Roles<W, ENC_ONLY, SUBF == CM>::THREADS, 1)
         const int64_t row = tile * BR + rl;
         const uint32_t* myc = s_codes + (b * BR + rl) * CBW;
         uint32_t ae[W], ao[W];
+        if constexpr (TILED) {
+#pragma unroll 1
+          for (int t = 0; t < p.ntile; ++t) {
+            scan_core<C, W, U, false, 0>(s_lut + (size_t)t * C * W * 16, [&](int g) { return myc[g]; }, ae, ao);
+            if (row < p.N)
+              store_row<W, false>(p.out + row * p.ldo + 4 * W * t, p.M - 4 * W * t, ae, ao, p.alpha_eff,
+                                  p.beta32, p.pair);
+          }
+          if (k == KR - 1) mbar_arrive(&cempty[b]);
+          continue;
+        }
         if constexpr (PROBE) {
 #pragma unroll
           for (int w = 0; w < W; ++w) ae[w] = 0u, ao[w] = 0u;
@@ -487,6 +518,49 @@ __global__ void __launch_bounds__(256) k_scan_fast(const uint32_t* __restrict__ 
   }
 }
 
+// mdn_scan for table widths without a compiled kernel: the tables cut into
+// ntile column tiles of WT words ([tile][c][WT][16] in shared memory, words
+// past the width zero); a thread's row walks the tiles with its code words
+// in registers.
+template <int C, int WT, int U>
+__global__ void __launch_bounds__(256) k_scan_tiled(const uint32_t* __restrict__ lut_g, int Wfull,
+                                                    int ntile, const uint8_t* __restrict__ codes,
+                                                    int64_t N, int M, int32_t* __restrict__ sums,
+                                                    float* __restrict__ out, int64_t ldo, float a,
+                                                    float b, int scale, bool pair, bool vec_codes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
+  const int n = ntile * C * WT * 16;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int k = i & 15, w = (i >> 4) % WT, c = (i / (16 * WT)) % C, t = i / (16 * WT * C);
+    const int gw = t * WT + w;
+    s_lut[i] = gw < Wfull ? lut_g[((size_t)c * Wfull + gw) * 16 + k] : 0u;
+  }
+  __syncthreads();
+  constexpr int NW = C >= 8 ? C / 8 : 1;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < N;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t cw[NW];
+    load_code_words<C>(codes, row, cw, vec_codes);
+#pragma unroll 1
+    for (int t = 0; t < ntile; ++t) {
+      uint32_t ae[WT], ao[WT];
+      scan_core<C, WT, U, false, 0>(
+          s_lut + (size_t)t * C * WT * 16,
+          [&](int g) {
+            uint32_t r = cw[0];
+#pragma unroll
+            for (int q = 1; q < NW; ++q) r = g == q ? cw[q] : r;
+            return r;
+          },
+          ae, ao);
+      const int m0 = 4 * WT * t;
+      if (sums) store_sums<WT>(sums + row * M + m0, M - m0, scale, ae, ao);
+      if (out) store_row<WT, false>(out + row * ldo + m0, M - m0, ae, ao, a, b, pair);
+    }
+  }
+}
+
 // ------------------------------------------------------------ host side --
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -555,7 +629,7 @@ struct Geometry {
 // 16 bytes of padding) fits the 256-element TMA box limit and is a multiple of
 // 16 bytes; then the largest rows-per-stage R (dividing the 256-row tile) that
 // leaves room for >= 4 stages (>= 2 at worst). es = input element size.
-Geometry plan(int C, int W, int D, bool enc_only, int es) {
+Geometry plan(int C, int W, int D, bool enc_only, int es, int ntile) {
   Geometry g;
   const int pad_e = 16 / es;
   if (D % pad_e != 0) return g;
@@ -571,7 +645,7 @@ Geometry plan(int C, int W, int D, bool enc_only, int es) {
   g.pad_e = pad_e;
   const int CBW = C >= 8 ? C / 8 : 1;
   size_t fixed = BAR_BYTES + thr_base(C) * 4 + off_base(C) * 4 + C * 4 + 16;
-  if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4;
+  if (!enc_only) fixed += (size_t)C * W * 16 * 4 * ntile + (size_t)NB * BR * CBW * 4;
   fixed = (fixed + 127) & ~size_t(127);
   const size_t budget = (size_t)dev_info().smem_optin;
   const int align_e = 128 / es;
@@ -638,13 +712,14 @@ bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <class TIn, int C, int W, int U, bool VEC, bool ENC, int SUBF, bool PROBE = false>
+template <class TIn, int C, int W, int U, bool VEC, bool ENC, int SUBF, bool PROBE = false,
+          bool TILED = false>
 cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
-  auto k = k_amm_ws<TIn, C, W, U, VEC, ENC, SUBF, PROBE>;
+  auto k = k_amm_ws<TIn, C, W, U, VEC, ENC, SUBF, PROBE, TILED>;
   cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (attr_err != cudaSuccess) return attr_err;
   int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
-  k<<<(unsigned)grid, Roles<W, ENC, SUBF == CM>::THREADS, smem, s>>>(tm, p);
+  k<<<(unsigned)grid, Roles<(TILED ? 8 : W), ENC, SUBF == CM>::THREADS, smem, s>>>(tm, p);
   return cudaGetLastError();
 }
 
@@ -735,7 +810,22 @@ static bool amm_fast_ok(const TreesDev& t, const LutsDev& l, const void* A, int6
   if (!has_combo(t.C, l.W, l.U)) return false;
   if (!aligned16(A) || (lda * es) % 16 != 0) return false;
   if (!encode_fn()) return false;
-  *geo = plan(t.C, l.W, t.D, false, es);
+  *geo = plan(t.C, l.W, t.D, false, es, 1);
+  return geo->ok;
+}
+
+// Table widths without a compiled kernel: the tile width with a compiled
+// (C, WT, U) kernel (4 words = 16 columns for C >= 16) and the tile count;
+// false if no tiled kernel serves these shapes (the generic kernel then runs).
+static bool tiled_plan(const TreesDev& t, const LutsDev& l, const void* A, int64_t lda, int es,
+                       int* WT, int* ntile, Geometry* geo) {
+  if (has_combo(t.C, l.W, l.U) || es != 4) return false;
+  const int wt = t.C >= 16 ? 4 : (t.C == 8 ? 2 : (t.C == 4 ? 1 : 0));
+  if (!wt || !has_combo(t.C, wt, l.U) || l.W <= wt) return false;
+  if (!aligned16(A) || (lda * es) % 16 != 0 || !encode_fn()) return false;
+  *WT = wt;
+  *ntile = (l.W + wt - 1) / wt;
+  *geo = plan(t.C, wt, t.D, false, es, *ntile);
   return geo->ok;
 }
 
@@ -744,7 +834,10 @@ const char* amm_variant_name(const TreesDev& t, const LutsDev& l, const float* A
   Geometry g;
   if (rt_enabled() && amm_rt_applies(t, l, 4))
     return (l.M == 2 || l.M == 4) && ldo % l.M == 0 ? "rt_vec" : "rt";
-  if (!amm_fast_ok(t, l, A, lda, 4, &g)) return "generic";
+  if (!amm_fast_ok(t, l, A, lda, 4, &g)) {
+    int wt, nt;
+    return tiled_plan(t, l, A, lda, 4, &wt, &nt, &g) ? "ws_tma_tiled" : "generic";
+  }
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
   static const char* names[2][3] = {{"ws_tma", "ws_tma_sub4", "ws_tma_sub8"},
                                     {"ws_tma_vec", "ws_tma_vec_sub4", "ws_tma_vec_sub8"}};
@@ -777,13 +870,54 @@ static Params base_params(const TreesDev& t, const Geometry& g, int64_t N) {
   return p;
 }
 
+// Tiled fused kernel for table widths without a compiled kernel (fp32 rows).
+static cudaError_t amm_tiled(const TreesDev& t, const LutsDev& l, const float* A, int64_t N,
+                             int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done) {
+  *done = false;
+  Geometry g;
+  int wt = 0, nt = 0;
+  if (!tiled_plan(t, l, A, lda, 4, &wt, &nt, &g)) return cudaSuccess;
+  CUtensorMap tm;
+  if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R, 4)) return cudaSuccess;
+  Params p = base_params(t, g, N);
+  const int sf = subf_for(t, g, 4);
+  p.ldo = ldo;
+  p.M = l.M;
+  p.pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
+  p.alpha_eff = l.alpha_eff;
+  p.beta32 = l.beta32;
+  p.lut = l.words;
+  p.out = out;
+  p.ntile = nt;
+  p.Wfull = l.W;
+  *done = true;
+#define TL(c, w, u, sfv)                                                                  \
+  if (t.C == c && wt == w && l.U == u && sf == sfv)                                       \
+    return launch_ws_sf<float, c, w, u, false, false, sfv, false, true>(tm, p, g.smem, s);
+  TL(4, 1, 0, 0) TL(4, 1, 4, 0) TL(4, 1, 0, 1) TL(4, 1, 4, 1) TL(4, 1, 0, 2) TL(4, 1, 4, 2)
+  TL(8, 2, 0, 0) TL(8, 2, 8, 0) TL(8, 2, 0, 1) TL(8, 2, 8, 1) TL(8, 2, 0, 2) TL(8, 2, 8, 2)
+#undef TL
+  // C >= 16: the per-split-dim encoder (SUBF 0) serves every subspace layout
+#define TL(c, w, u)                                                                      \
+  if (t.C == c && wt == w && l.U == u)                                                   \
+    return launch_ws_sf<float, c, w, u, false, false, 0, false, true>(tm, p, g.smem, s);
+  TL(16, 4, 0) TL(16, 4, 16) TL(32, 4, 0) TL(32, 4, 16) TL(64, 4, 0) TL(64, 4, 16)
+#undef TL
+  *done = false;
+  return cudaSuccess;
+}
+
 template <class TIn>
 static cudaError_t amm_fast(const TreesDev& t, const LutsDev& l, const TIn* A, int64_t N,
                             int64_t lda, float* out, int64_t ldo, cudaStream_t s, bool* done) {
   constexpr int es = sizeof(TIn);
   *done = false;
   Geometry g;
-  if (N > (int64_t)0x7FFFFF00 || !amm_fast_ok(t, l, A, lda, es, &g)) return cudaSuccess;
+  if (N > (int64_t)0x7FFFFF00) return cudaSuccess;
+  if (!amm_fast_ok(t, l, A, lda, es, &g)) {
+    if constexpr (es == 4) return amm_tiled(t, l, A, N, lda, out, ldo, s, done);
+    return cudaSuccess;
+  }
   CUtensorMap tm;
   if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R, es)) return cudaSuccess;
   Params p = base_params(t, g, N);
@@ -852,7 +986,7 @@ static cudaError_t encode_fast(const TreesDev& t, const TIn* A, int64_t N, int64
     return cudaSuccess;
   if (t.C >= 8 && (reinterpret_cast<uintptr_t>(codes) & 3u)) return cudaSuccess;
   if (t.C == 4 && (reinterpret_cast<uintptr_t>(codes) & 1u)) return cudaSuccess;
-  Geometry g = plan(t.C, 1, t.D, true, es);
+  Geometry g = plan(t.C, 1, t.D, true, es, 1);
   if (!g.ok) return cudaSuccess;
   CUtensorMap tm;
   if (!make_tmap(&tm, A, N, lda, t.D, g.SW, g.R, es)) return cudaSuccess;
@@ -1038,7 +1172,39 @@ cudaError_t launch_scan(const LutsDev& l, const uint8_t* codes, int64_t N, int32
                         float* out, int64_t ldo, cudaStream_t s) {
   const bool codes_ok = l.C >= 8 ? (reinterpret_cast<uintptr_t>(codes) & 3u) == 0
                                  : (reinterpret_cast<uintptr_t>(codes) & 1u) == 0;
-  if (!has_combo(l.C, l.W, l.U) || !codes_ok) return launch_scan_generic(l, codes, N, sums, out, ldo, s);
+  if (!codes_ok) return launch_scan_generic(l, codes, N, sums, out, ldo, s);
+  if (!has_combo(l.C, l.W, l.U)) {
+    const int wt = l.C >= 16 ? 4 : (l.C == 8 ? 2 : (l.C == 4 ? 1 : 0));
+    if (wt && has_combo(l.C, wt, l.U) && l.W > wt) {
+      const int nt = (l.W + wt - 1) / wt;
+      const size_t smem = (size_t)nt * l.C * wt * 16 * 4;
+      if (smem <= (size_t)dev_info().smem_optin) {
+        auto launch_tiled = [&](auto kern) -> cudaError_t {
+          cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), smem);
+          if (e != cudaSuccess) return e;
+          int per_sm = 0;
+          e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+          if (e != cudaSuccess) return e;
+          if (per_sm < 1) per_sm = 1;
+          int64_t blocks = (N + 255) / 256;
+          const int64_t cap = (int64_t)dev_info().sms * per_sm;
+          if (blocks > cap) blocks = cap;
+          const bool pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
+          const bool vec_codes = (reinterpret_cast<uintptr_t>(codes) & (l.C == 32 ? 15u : 7u)) == 0;
+          kern<<<(unsigned)blocks, 256, smem, s>>>(l.words, l.W, nt, codes, N, l.M, sums, out, ldo,
+                                                   l.alpha_eff, l.beta32, l.U == 0 ? 1 : l.U, pair,
+                                                   vec_codes);
+          return cudaGetLastError();
+        };
+#define TS(c, w, u) \
+        if (l.C == c && wt == w && l.U == u) return launch_tiled(k_scan_tiled<c, w, u>);
+        TS(4, 1, 0) TS(4, 1, 4) TS(8, 2, 0) TS(8, 2, 8) TS(16, 4, 0) TS(16, 4, 16)
+        TS(32, 4, 0) TS(32, 4, 16) TS(64, 4, 0) TS(64, 4, 16)
+#undef TS
+      }
+    }
+    return launch_scan_generic(l, codes, N, sums, out, ldo, s);
+  }
   const bool vec = out && l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
 #define X(c, w, u)                                                                  \
   if (l.C == c && l.W == w && l.U == u)                                             \
