@@ -475,12 +475,22 @@ __device__ __forceinline__ void load_code_words(const uint8_t* __restrict__ code
   }
 }
 
+// k_scan_fast's body; two entry points that differ only in their launch
+// bounds. __launch_bounds__(256, 1) lets ptxas keep the wide tables' row in
+// registers (cls100: 99 -> 127 registers, 2 blocks/SM) and schedule more
+// lookups ahead; it pays for the wide tables and costs the narrow ones
+// (same box, rows/s: cls100 5.05 -> 5.51e9, cls10_c64 2.15 -> 2.23e10, but
+// scale 3.57 -> 3.24e10, image 2.46 -> 2.39e11, cls10_c16 and tiny flat).
+template <int C, int W>
+constexpr bool scan_lb1() {
+  return W >= 8 || C >= 64;
+}
 template <int C, int W, int U, bool VEC, int MIX>
-__global__ void __launch_bounds__(256) k_scan_fast(const uint32_t* __restrict__ lut_g,
-                                                   const uint8_t* __restrict__ codes, int64_t N,
-                                                   int M, int32_t* __restrict__ sums,
-                                                   float* __restrict__ out, int64_t ldo, float a,
-                                                   float b, int scale, bool pair, bool vec_codes) {
+__device__ __forceinline__ void scan_fast_body(const uint32_t* __restrict__ lut_g,
+                                               const uint8_t* __restrict__ codes, int64_t N, int M,
+                                               int32_t* __restrict__ sums, float* __restrict__ out,
+                                               int64_t ldo, float a, float b, int scale, bool pair,
+                                               bool vec_codes) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
   for (int i = threadIdx.x; i < C * W * 4; i += blockDim.x)
@@ -517,6 +527,20 @@ __global__ void __launch_bounds__(256) k_scan_fast(const uint32_t* __restrict__ 
     }
   }
 }
+
+#define MDN_SCAN_ARGS                                                                         \
+  const uint32_t *__restrict__ lut_g, const uint8_t *__restrict__ codes, int64_t N, int M,     \
+      int32_t *__restrict__ sums, float *__restrict__ out, int64_t ldo, float a, float b,       \
+      int scale, bool pair, bool vec_codes
+template <int C, int W, int U, bool VEC, int MIX>
+__global__ void __launch_bounds__(256) k_scan_fast(MDN_SCAN_ARGS) {
+  scan_fast_body<C, W, U, VEC, MIX>(lut_g, codes, N, M, sums, out, ldo, a, b, scale, pair, vec_codes);
+}
+template <int C, int W, int U, bool VEC, int MIX>
+__global__ void __launch_bounds__(256, 1) k_scan_fast_lb1(MDN_SCAN_ARGS) {
+  scan_fast_body<C, W, U, VEC, MIX>(lut_g, codes, N, M, sums, out, ldo, a, b, scale, pair, vec_codes);
+}
+#undef MDN_SCAN_ARGS
 
 // mdn_scan for table widths without a compiled kernel: the tables cut into
 // ntile column tiles of WT words ([tile][c][WT][16] in shared memory, words
@@ -746,9 +770,18 @@ static int scan_mix(int C) {
 template <int C, int W, int U, bool VEC>
 cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int32_t* sums,
                           float* out, int64_t ldo, cudaStream_t s) {
-  auto k = k_scan_fast<C, W, U, VEC, 0>;
-  if constexpr (U == 0)
-    if (scan_mix(C) == 3) k = k_scan_fast<C, W, U, VEC, 3>;
+  using KFn = void (*)(const uint32_t*, const uint8_t*, int64_t, int, int32_t*, float*, int64_t, float,
+                      float, int, bool, bool);
+  KFn k;
+  if constexpr (scan_lb1<C, W>()) {
+    k = k_scan_fast_lb1<C, W, U, VEC, 0>;
+    if constexpr (U == 0)
+      if (scan_mix(C) == 3) k = k_scan_fast_lb1<C, W, U, VEC, 3>;
+  } else {
+    k = k_scan_fast<C, W, U, VEC, 0>;
+    if constexpr (U == 0)
+      if (scan_mix(C) == 3) k = k_scan_fast<C, W, U, VEC, 3>;
+  }
   size_t smem = (size_t)C * W * 16 * 4;
   cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (attr_err != cudaSuccess) return attr_err;

@@ -152,6 +152,8 @@ struct ByteTree {
   uint32_t s0, s1, s2, s3;         // PRMT selectors of the split values in the subspace word
   uint32_t g2, g3;                 // byte 0 of Q2 / Q3lo (pad bytes of the packed compares)
   uint32_t base;                   // table address of code 15 (n_4 = 0)
+  uint32_t oh[4];                  // dp4a forms: one-hot byte of split dim t in the subspace word
+  uint32_t nq0, nd12, nq2;         // -q0, -(q1 - q2), -q2
 };
 
 // Raw PRMT / shift: __byte_perm masks its selector (LOP3 & 0x7777) to hide
@@ -178,6 +180,34 @@ __device__ __forceinline__ uint32_t push_sign(uint32_t n, uint32_t d) {
 #ifndef MDN_BQ01
 #define MDN_BQ01 1   // levels 0 and 1 from one PRMT (x1 + (x0 << 16)); 0: one PRMT each
 #endif
+// Byte-tree levels in the dp4a form (template DP, a bitmask; bit 0: levels 0+1,
+// bit 1: level 2, bit 2: level 3): x_j - v as dp4a(w, onehot_j, -v) or
+// dp4a(V, -1 @ byte 0, x_j) on the FMA pipe instead of PRMT + subtract on the
+// ALU pipe, which the byte trees saturate. Same-box A/B (rows/s, image_u8):
+// fused 0: 1.364e11, 6: 1.375e11, 7: 1.255e11 (the FMA pipe then carries the
+// scan's adds as well); encode-only 0: 1.414e11, 4: 1.483e11, 6: 1.475e11,
+// 7: 1.495e11. MDN_BQ_DP (build flag) forces one form for A/B.
+template <bool ENC>
+constexpr int bq_dp() {
+#ifdef MDN_BQ_DP
+  return MDN_BQ_DP;
+#else
+  return ENC ? 7 : 6;
+#endif
+}
+
+// x_j - v on the FMA pipe: dp4a(w, onehot_j, c) = x_j + c, and
+// dp4a(V, 0x000000FF, x) = x - byte0(V) (signed b: -1 at byte 0, 0 elsewhere).
+__device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t dp4a_us(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
 static __constant__ uint32_t k_shift16 = 65536u;   // opaque to ptxas: the multiply stays an IMAD
 
 __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
@@ -191,23 +221,38 @@ __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
 // is negative iff x0 < q0 (x1 < 2^16 cannot carry into the sign), and
 // r * 2^16 - (v1 << 16) = (x1 - v1) << 16 has the sign of x1 - v1 (|x1 - v1|
 // < 2^8), both products on the FMA pipe.
+template <int DP>
 __device__ __forceinline__ uint32_t byte_tree_n4(uint32_t w, const ByteTree& b) {
+  uint32_t n2;
+  if constexpr ((DP & 1) != 0) {
+    // dp4a form: x0 - q0 and x1 - v1 (v1 = q2 + lt0 (q1 - q2)) as dp4a(w, onehot, -v)
+    const uint32_t lt0 = sign_bit(dp4a_uu(w, b.oh[0], b.nq0));
+    n2 = push_sign(lt0, dp4a_uu(w, b.oh[1], mad_lo(lt0, b.nd12, b.nq2)));
+  } else {
 #if MDN_BQ01
-  const uint32_t r = prmt(w, 0u, b.s01);
-  const uint32_t lt0 = sign_bit(r - b.q0s);
-  const uint32_t n2 = push_sign(lt0, mad_lo(r, k_shift16, mad_lo(lt0, b.nd12s, b.nq2s)));
+    const uint32_t r = prmt(w, 0u, b.s01);
+    const uint32_t lt0 = sign_bit(r - b.q0s);
+    n2 = push_sign(lt0, mad_lo(r, k_shift16, mad_lo(lt0, b.nd12s, b.nq2s)));
 #else
-  const uint32_t lt0 = sign_bit(prmt(w, 0u, b.s0) - (uint32_t)b.q0);
-  const uint32_t v1 = (uint32_t)b.q2 + lt0 * (uint32_t)b.d12;
-  const uint32_t n2 = push_sign(lt0, prmt(w, 0u, b.s1) - v1);
+    const uint32_t lt0 = sign_bit(prmt(w, 0u, b.s0) - (uint32_t)b.q0);
+    const uint32_t v1 = (uint32_t)b.q2 + lt0 * (uint32_t)b.d12;
+    n2 = push_sign(lt0, prmt(w, 0u, b.s1) - v1);
 #endif
-  const uint32_t n3 = push_sign(n2, prmt(w, b.g2, b.s2) - prmt(b.Q2, b.Q2, n2));
-  return push_sign(n3, prmt(w, b.g3, b.s3) - prmt(b.Q3lo, b.Q3hi, n3));
+  }
+  uint32_t n3;
+  if constexpr ((DP & 2) != 0)
+    n3 = push_sign(n2, dp4a_us(prmt(b.Q2, b.Q2, n2), 0x000000FFu, dp4a_uu(w, b.oh[2], 0u)));
+  else
+    n3 = push_sign(n2, prmt(w, b.g2, b.s2) - prmt(b.Q2, b.Q2, n2));
+  if constexpr ((DP & 4) != 0)
+    return push_sign(n3, dp4a_us(prmt(b.Q3lo, b.Q3hi, n3), 0x000000FFu, dp4a_uu(w, b.oh[3], 0u)));
+  else
+    return push_sign(n3, prmt(w, b.g3, b.s3) - prmt(b.Q3lo, b.Q3hi, n3));
 }
 
 template <int W2>
 __device__ __forceinline__ uint32_t byte_tree_addr(uint32_t w, const ByteTree& b) {
-  return b.base - byte_tree_n4(w, b) * (4u * W2 * lanes_lut<uint8_t>());   // 15 - n4 = code
+  return b.base - byte_tree_n4<bq_dp<false>()>(w, b) * (4u * W2 * lanes_lut<uint8_t>());   // 15 - n4 = code
 }
 
 // mu(a, b) = floor((a + b + 1) / 2) on two 16-bit lanes holding values < 256
@@ -346,6 +391,10 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
     bt.s2 = j2 | 0x4440u;                          // (x, g, g, g)
     bt.s3 = j3 | 0x4440u;
     bt.base = lut_c + 15u * 4u * W2 * LANES_LUT;
+    bt.oh[0] = 1u << (8 * j0), bt.oh[1] = 1u << (8 * j1), bt.oh[2] = 1u << (8 * j2), bt.oh[3] = 1u << (8 * j3);
+    bt.nq0 = 0u - (uint32_t)bt.q0;
+    bt.nd12 = 0u - (uint32_t)bt.d12;
+    bt.nq2 = 0u - (uint32_t)bt.q2;
   }
   // ENC transpose constants: stage k exchanges with lane c ^ 2^k; a lane whose
   // bit k is b keeps the nibbles whose index has bit k == b and receives the
@@ -388,7 +437,7 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
 #pragma unroll
       for (int it = 0; it < C; ++it) {
         if constexpr (BQ && ENC)
-          code[it] = 15u - byte_tree_n4(w[it], bt);
+          code[it] = 15u - byte_tree_n4<bq_dp<true>()>(w[it], bt);
         else if constexpr (BQ)
           code[it] = byte_tree_addr<W2>(w[it], bt) + (LANE_LUT ? 4u * RPW * it : 0u);
         else
