@@ -106,12 +106,11 @@ struct SParams {
 };
 
 // Code rows are C words (one table address per codebook). C = 8: rows whose
-// index has bit 2 set store their two 16-B halves swapped (word c ^ 4), so the
-// encoder's stores (4 rows x 8 codebooks) and the scanner's lane-per-row
-// LDS.128 reads (a quarter-warp = rows 8k..8k+7) both cover all 32 banks
-// once. The scanner then sees codebook c ^ 4 in slot c: harmless for the exact
-// sum, and for the App. D averaging tree over the 8 codebooks an XOR of the
-// leaf index only swaps the (commutative) operands of some mu(a, b).
+// index has bit 2 set store their two 16-B halves swapped (word c ^ 4), and
+// the scanner's lane-per-row LDS.128 reads apply the same swizzle, so the
+// encoder's stores (4 rows x 8 codebooks) and the reads (a quarter-warp =
+// rows 8k..8k+7) both cover all 32 banks once, and every lane sees its
+// codebooks in order.
 template <int C>
 struct CodeStride {
   static constexpr int value = C;
@@ -494,7 +493,10 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
     uint32_t off[C];
 #pragma unroll
     for (int k = 0; k < C; k += 4) {
-      const uint4 v = *reinterpret_cast<const uint4*>(s_code + lane * CS + k);
+      // read with the store's swizzle: a quarter-warp's 8 rows then cover the 32
+      // banks once (unswizzled reads of rows r and r + 4 hit the same 4 banks:
+      // ncu, image_u8: 8 wavefronts per LDS.128 for an ideal 4)
+      const uint4 v = *reinterpret_cast<const uint4*>(s_code + lane * CS + (C == 8 ? (k ^ (lane & 4)) : k));
       off[k] = v.x, off[k + 1] = v.y, off[k + 2] = v.z, off[k + 3] = v.w;
     }
     __syncwarp();                                    // s_code may be rewritten next stage

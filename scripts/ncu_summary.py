@@ -35,7 +35,9 @@ METRICS = [
     "smsp__warps_eligible.avg.per_cycle_active",
     "lts__t_sector_hit_rate.pct", "launch__registers_per_thread", "launch__grid_size",
     "launch__block_size", "launch__shared_mem_per_block_dynamic", "sm__cycles_elapsed.avg.per_second",
-]
+] + [f"smsp__average_warps_issue_stalled_{r}_per_issue_active.ratio" for r in (
+    "math_pipe_throttle", "mio_throttle", "long_scoreboard", "short_scoreboard", "wait",
+    "not_selected", "barrier", "lg_throttle", "membar", "sleeping")]
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "us": 1e-6, "ms": 1e-3, "ns": 1e-9,
          "s": 1.0, "Ghz": 1e9, "Mhz": 1e6}
 
