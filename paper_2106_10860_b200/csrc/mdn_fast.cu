@@ -42,8 +42,9 @@ namespace fast {
 
 constexpr int BR = 256;                  // rows per tile
 constexpr int NB = 3;                    // code ring depth (tiles)
-constexpr int NS_MAX = 8;                // A stage ring depth cap
-constexpr int BAR_BYTES = 256;
+constexpr int NS_MAX = 16;               // A stage ring depth cap
+constexpr int BAR_BYTES = 384;           // full/empty[NS_MAX] + cfull/cempty[NB] mbarriers
+static_assert((2 * NS_MAX + 2 * NB) * 8 <= BAR_BYTES, "mbarriers must fit below the tables");
 constexpr int CM = -1;                   // SUBF value of the column-major-A variant
 
 // Shared-memory word offsets of codebook c's 16 thresholds / 4 split offsets.
@@ -643,6 +644,8 @@ DevInfo dev_info() {
   return di;
 }
 
+int env_int(const char* name, int dflt);
+
 struct Geometry {
   bool ok = false;
   int SW, nslab, R, NS, slab_e, pad_e;
@@ -673,8 +676,11 @@ Geometry plan(int C, int W, int D, bool enc_only, int es, int ntile) {
   fixed = (fixed + 127) & ~size_t(127);
   const size_t budget = (size_t)dev_info().smem_optin;
   const int align_e = 128 / es;
-  for (int min_ns : {4, 2}) {
+  static const int rmax = env_int("MDN_WS_RMAX", 256);   // A/B knob: cap on rows per stage
+  static const int mns = env_int("MDN_WS_MINNS", 3);     // fewest stages for the largest R (A/B knob)
+  for (int min_ns : {mns, 2}) {
     for (int R : {256, 128, 64, 32, 16, 8}) {
+      if (R > rmax) continue;
       int slab_e = ((R * (g.SW + pad_e)) + align_e - 1) / align_e * align_e;
       size_t stage = (size_t)nslab * slab_e * es;
       if (fixed + stage * min_ns > budget) continue;
