@@ -10,6 +10,8 @@ bash scripts/ncu_capture.sh \
   tiny_exact k_amm_rt --config tiny -- \
   image_exact k_amm_rt --config image -- \
   image_u8_exact k_amm_rt --config image_u8 -- \
+  image_u8_avg k_amm_rt --config image_u8 --mode avg -- \
+  cls10_c64_scan_exact k_scan_fast --config cls10_c64 --op scan -- \
   cls100_col_exact k_amm_ws --config cls100 --layout col -- \
   scale_col_exact k_amm_ws --config scale --layout col -- \
   tiny_col_exact k_amm_cm --config tiny --layout col -- \
