@@ -39,6 +39,11 @@ struct TreesDev {
   int n_cols;
   const float* pq_cent;  // PQ model: prototypes [16][DS/4][C][4] (equal subspaces), or null
   int pq_ds;             // PQ subspace width DS of pq_cent (0 if null)
+  // Host copies (the model's): launchers that pass per-codebook constants as
+  // kernel parameters read them here.
+  const uint16_t* h_dims = nullptr;
+  const uint16_t* h_sub = nullptr;
+  const uint16_t* h_q = nullptr;
 };
 
 // Quantised tables as the kernels consume them (device).
@@ -143,7 +148,8 @@ struct mdn_model {
   float* d_P = nullptr;           // [16C][D]
   mdn::TreesDev trees() const {
     return {d_dims, d_thr, d_sub, d_q, C, D, subf, subf_u8, q_byte, d_cols, d_slot,
-            (int)h_cols.size(), d_pqcent, d_pqcent ? pq_ds : 0};
+            (int)h_cols.size(), d_pqcent, d_pqcent ? pq_ds : 0,
+            h_dims.data(), h_sub.data(), h_q.data()};
   }
 };
 

@@ -559,6 +559,321 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_u8_rows: the 8-bit byte-tree path with lane = row for BOTH halves.
+//
+// k_amm_rt maps lane -> (row, codebook) for the encode so that each lane keeps
+// one codebook's tree in registers, and then hands the codes to lane -> row
+// for the scan through a shared buffer (per 32 rows and C = 8: 8 word loads,
+// 8 code stores, 2 x LDS.128 back, two __syncwarp; encode-only: a 3-stage
+// nibble transpose). For 8-bit rows whose codebooks are the 4-byte words of
+// the row (App. B; image_u8) all of that can go: the lane loads its own
+// 32-byte row (2 x LDS.128) and walks all C trees itself. The trees' byte
+// tables and selectors are the same for every lane, so they are kernel
+// parameters (constant bank operands of PRMT / IMAD / IDP4A) rather than
+// per-lane registers; only the PRMT sources Q2, Q3lo, Q3hi need registers.
+// Per (row, codebook) the encode is the same byte tree as k_amm_rt (one PRMT
+// per level picks the node's split value; sign-bit
+// compares, Alg. 1), the table address one IMAD, the lookup one LDS.
+// Encode-only: the row's codes pack into one register (no transpose) and leave
+// in one coalesced 4-byte store per lane.
+// Stage ring cap (8 KB stages). Same-box A/B (exact / avg / encode rows/s):
+// 16 stages 1.400 / 1.273 / 1.552e11, 24: 1.377 / 1.271 / 1.521e11, 32:
+// 1.377 / 1.273 / 1.501e11 -- not bound by bytes in flight.
+#ifndef MDN_U8ROWS_NS_MAX
+#define MDN_U8ROWS_NS_MAX 16
+#endif
+constexpr int U8_NS_MAX = MDN_U8ROWS_NS_MAX;
+struct RParams {
+  SParams p;
+  ByteTree cb[8];   // per codebook; ByteTree::base unused (lane-independent)
+};
+
+template <int C, int W2, int U, int VEC, bool ENC, int DP, int SUBS>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_u8_rows(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ RParams rp) {
+  static_assert(C == 8, "codebooks are the 4-byte words of a 32-byte row");
+  constexpr int D = 32;
+  constexpr int CPS = R / (32 * SUBS), NG = NWK / CPS;
+  constexpr int LROW = 128;                        // bytes per (c, k, w) table row: 32 lanes
+  constexpr int OFF_LUT = 16 * U8_NS_MAX;          // full / empty barriers below
+  constexpr int OFF_STAGE = (OFF_LUT + (ENC ? 0 : C * 16 * W2 * LROW) + 127) & ~127;
+  const SParams& p = rp.p;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + U8_NS_MAX;
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + OFF_LUT);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  // per-lane replicated tables: word (c, k, w) of lane l at ((c 16 + k) W2 + w) 32 + l
+  if constexpr (!ENC)
+    for (int i = tid; i < C * 16 * W2 * 32; i += blockDim.x) s_lut[i] = p.lut16[i >> 5];
+  if (tid == 0) {
+    for (int s = 0; s < p.NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  __syncthreads();
+  const int n_local = (int)((p.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(R * D);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int q = 0; q < n_local; ++q) {
+        mbar_wait_sleep(&empty[s], ph ^ 1u);
+        mbar_arrive_tx(&full[s], bytes);
+        const int64_t y = (blockIdx.x + q * gridDim.x) * (int64_t)R;
+        tma_load_2d(smem + OFF_STAGE + (size_t)s * p.stage_b, &tmap, 0, (int)y, &full[s], 0, 0);
+        if (++s == p.NS) s = 0, ph ^= 1u;
+      }
+    }
+    return;
+  }
+
+  const int wk = warp - 1;
+  const int grp = wk / CPS, chunk = wk % CPS;
+  // table address of (c, k = 15, w = 0) for this lane; code k = 15 - n4
+  const uint32_t lbase = su32(s_lut) + 4u * (uint32_t)lane + 15u * W2 * LROW;
+  int s = grp, ph = 0;
+  while (s >= p.NS) s -= p.NS, ph ^= 1;
+  uint32_t row = ((uint32_t)blockIdx.x + (uint32_t)grp * gridDim.x) * R + chunk * 32 * SUBS + lane;
+  const uint32_t row_step = (uint32_t)NG * gridDim.x * R;
+  const uint32_t n_rows = (uint32_t)p.N;
+  float* o_row = p.out + (int64_t)row * p.ldo;
+  const int64_t o_step = (int64_t)row_step * p.ldo;
+  const float alpha = p.alpha_eff, beta = p.beta32;
+
+  for (int q = grp; q < n_local; q += NG, row += row_step, o_row += o_step) {
+    mbar_wait_sleep(&full[s], (uint32_t)ph);
+#pragma unroll 1
+    for (int hs = 0; hs < SUBS; ++hs) {
+      const unsigned char* rp_row =
+          smem + OFF_STAGE + (size_t)s * p.stage_b + (size_t)(chunk * 32 * SUBS + hs * 32 + lane) * D;
+      const uint4 lo = *reinterpret_cast<const uint4*>(rp_row);
+      const uint4 hi = *reinterpret_cast<const uint4*>(rp_row + 16);
+      const uint32_t xw[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+      // The rows now live in registers: release the slot before the compute
+      // (the arrive's release semantics order the warp's loads before it).
+      __syncwarp();
+      if (hs == SUBS - 1 && lane == 0) mbar_arrive(&empty[s]);
+      uint32_t n4[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) n4[c] = byte_tree_n4<DP>(xw[c], rp.cb[c]);
+      const uint32_t r = row + hs * 32;
+      if constexpr (ENC) {
+        // packed codes, low nibble = codebook 0 (L147 / L608): sum_c (15 - n4_c) 16^c
+        uint32_t acc = n4[0];
+#pragma unroll
+        for (int c = 1; c < C; ++c) acc = mad_lo(n4[c], 1u << (4 * c), acc);
+        if (r < n_rows) reinterpret_cast<uint32_t*>(p.codes)[r] = ~acc;
+        continue;
+      }
+      uint32_t addr[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) addr[c] = mad_lo(n4[c], 0u - (uint32_t)(W2 * LROW), lbase);
+      uint32_t acc[W2];
+#pragma unroll
+      for (int w = 0; w < W2; ++w) acc[w] = 0u;
+      if constexpr (U == 0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+#pragma unroll
+          for (int w = 0; w < W2; ++w) acc[w] += lds_u32(addr[c] + (uint32_t)((c * 16 * W2 + w) * LROW));
+      } else {
+        static_assert((U & (U - 1)) == 0 && C % U == 0, "U must be a power of two dividing C");
+#pragma unroll
+        for (int blk = 0; blk < C / U; ++blk)
+#pragma unroll
+          for (int w = 0; w < W2; ++w) {
+            uint32_t v[U];
+#pragma unroll
+            for (int i = 0; i < U; ++i) {
+              const int c = blk * U + i;
+              v[i] = lds_u32(addr[c] + (uint32_t)((c * 16 * W2 + w) * LROW));
+            }
+#pragma unroll
+            for (int st = 1; st < U; st *= 2)          // halves recursion = adjacent pairs (R17)
+#pragma unroll
+              for (int i = 0; i < U; i += 2 * st) v[i] = avg16(v[i], v[i + st]);
+            acc[w] += v[0];
+          }
+      }
+      if (r < n_rows) {
+        float* o_h = o_row + (int64_t)hs * 32 * p.ldo;
+        float f[2 * W2];
+#pragma unroll
+        for (int w = 0; w < W2; ++w) {
+          f[2 * w] = __fmaf_rn(alpha, u16_to_f(acc[w] & 0xFFFFu), beta);
+          f[2 * w + 1] = __fmaf_rn(alpha, u16_to_f(acc[w] >> 16), beta);
+        }
+        if constexpr (VEC) {
+          if constexpr (W2 % 2 == 0) {
+#pragma unroll
+            for (int w = 0; w < W2; w += 2)
+              *reinterpret_cast<float4*>(o_h + 2 * w) = make_float4(f[2 * w], f[2 * w + 1], f[2 * w + 2], f[2 * w + 3]);
+          } else {
+#pragma unroll
+            for (int w = 0; w < W2; ++w)
+              *reinterpret_cast<float2*>(o_h + 2 * w) = make_float2(f[2 * w], f[2 * w + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < 2 * W2; ++m)
+            if (m < p.M) o_h[m] = f[m];
+        }
+      }
+    }
+    s += NG;
+    if (s >= p.NS) s -= p.NS, ph ^= 1;
+  }
+}
+
+// The per-codebook byte-tree constants (as k_amm_rt's lanes build them, from
+// the model's host copies of the split dims, subspace starts and 8-bit split
+// values q, heap order).
+static void host_byte_tree(const TreesDev& t, int c, ByteTree* b) {
+  const uint16_t* qc = t.h_q + c * 16;
+  *b = ByteTree{};
+  b->q0 = qc[0];
+  b->q2 = qc[2];
+  b->d12 = (int)qc[1] - (int)qc[2];
+  for (int n = 0; n < 4; ++n) b->Q2 |= (uint32_t)qc[6 - n] << (8 * n);
+  for (int n = 0; n < 4; ++n) b->Q3lo |= (uint32_t)qc[14 - n] << (8 * n);
+  for (int n = 0; n < 4; ++n) b->Q3hi |= (uint32_t)qc[10 - n] << (8 * n);
+  b->g2 = b->Q2 & 0xFFu;
+  b->g3 = b->Q3lo & 0xFFu;
+  uint32_t j[4];
+  for (int l = 0; l < 4; ++l) j[l] = (uint32_t)(t.h_dims[c * 4 + l] - t.h_sub[c]);
+  b->s0 = j[0] | 0x4440u;
+  b->s1 = j[1] | 0x4440u;
+  b->s01 = j[1] | 0x40u | (j[0] << 8) | 0x4000u;
+  b->q0s = (uint32_t)b->q0 << 16;
+  b->nq2s = 0u - ((uint32_t)b->q2 << 16);
+  b->nd12s = 0u - ((uint32_t)b->d12 << 16);
+  b->s2 = j[2] | 0x4440u;
+  b->s3 = j[3] | 0x4440u;
+  b->base = 0u;
+  for (int l = 0; l < 4; ++l) b->oh[l] = 1u << (8 * j[l]);
+  b->nq0 = 0u - (uint32_t)b->q0;
+  b->nd12 = 0u - (uint32_t)b->d12;
+  b->nq2 = 0u - (uint32_t)b->q2;
+}
+
+// Per mode: 32-row chunks per stage wait (SUBS) and the byte-tree level forms
+// (DP, as bq_dp). Same-box A/B, image_u8 rows/s: exact SUBS 1 -> 2 1.24 ->
+// 1.40e11 (DP 7: 1.21 / 1.20e11); encode-only SUBS 2, DP 6 1.55e11 (SUBS 1
+// 1.36e11; DP 7 1.25e11); averaging SUBS 1, DP 7 1.39e11 (SUBS 2: DP 6
+// 1.27e11, DP 7 1.19e11). Build flags override (A/B only).
+#ifndef MDN_U8ROWS_SUBS
+#define MDN_U8ROWS_SUBS 2
+#endif
+#ifndef MDN_U8ROWS_SUBS_AVG
+#define MDN_U8ROWS_SUBS_AVG 1
+#endif
+#ifndef MDN_U8ROWS_SUBS_ENC
+#define MDN_U8ROWS_SUBS_ENC 2
+#endif
+#ifndef MDN_U8ROWS_DP
+#define MDN_U8ROWS_DP 6
+#endif
+#ifndef MDN_U8ROWS_DP_AVG
+#define MDN_U8ROWS_DP_AVG 7
+#endif
+#ifndef MDN_U8ROWS_DP_ENC
+#define MDN_U8ROWS_DP_ENC 6
+#endif
+template <bool ENC, int U>
+struct U8Cfg {
+  static constexpr int SUBS = ENC ? MDN_U8ROWS_SUBS_ENC : (U ? MDN_U8ROWS_SUBS_AVG : MDN_U8ROWS_SUBS);
+  static constexpr int DP = ENC ? MDN_U8ROWS_DP_ENC : (U ? MDN_U8ROWS_DP_AVG : MDN_U8ROWS_DP);
+  static constexpr int NG = NWK / (R / (32 * SUBS));   // worker groups rotating over stages
+};
+
+// Is k_u8_rows applicable? 8-bit rows of 32 bytes, 8 codebooks on the row's
+// 4-byte words, every split value a byte, host copies of the trees.
+static bool u8_rows_ok(const TreesDev& t) {
+  static const int on = env_int("MDN_U8_ROWS", 1);   // 0: k_amm_rt (A/B only)
+  return on != 0 && t.C == 8 && t.D == 32 && t.subf_u8 == 1 && t.q_byte && t.h_q && t.h_dims &&
+         t.h_sub;
+}
+
+template <int W2, int U, int VEC, bool ENC>
+static cudaError_t launch_u8_rows(const CUtensorMap& tm, const RParams& rp, size_t smem,
+                                  cudaStream_t st) {
+  using Cfg = U8Cfg<ENC, U>;
+  auto k = k_u8_rows<8, W2, U, VEC, ENC, Cfg::DP, Cfg::SUBS>;
+  cudaError_t e = ensure_smem(reinterpret_cast<const void*>(k), smem);
+  if (e != cudaSuccess) return e;
+  const int64_t cap = (int64_t)dev_info().sms;
+  const int64_t grid = rp.p.n_tiles < cap ? rp.p.n_tiles : cap;
+  k<<<(unsigned)grid, THREADS, smem, st>>>(tm, rp);
+  return cudaGetLastError();
+}
+
+// Fused (codes == nullptr) or encode-only (out == nullptr) 8-bit rows.
+static cudaError_t u8_rows(const TreesDev& t, const LutsDev* l, const uint8_t* A, int64_t N,
+                           int64_t lda, float* out, int64_t ldo, uint8_t* codes, cudaStream_t st,
+                           bool* done) {
+  *done = false;
+  const bool enc = codes != nullptr;
+  if (N > (int64_t)0x7FFFFF00 || !u8_rows_ok(t)) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(A) & 15u) || lda % 16) return cudaSuccess;
+  if (enc && (reinterpret_cast<uintptr_t>(codes) & 3u)) return cudaSuccess;
+  int W2 = 1;
+  if (!enc) {
+    if (l->M > 4 || !l->words16 || !(l->U == 0 || l->U == 8)) return cudaSuccess;
+    W2 = (l->M + 1) / 2;
+  }
+  const int stage_b = R * 32;
+  const size_t fixed = ((16 * U8_NS_MAX + (enc ? 0 : (size_t)8 * 16 * W2 * 128)) + 127) & ~size_t(127);
+  const size_t budget = (size_t)dev_info().smem_optin;
+  const bool avg = !enc && l->U != 0;
+  const int NG = enc ? U8Cfg<true, 0>::NG : (avg ? U8Cfg<false, 8>::NG : U8Cfg<false, 0>::NG);
+  if (fixed + (size_t)2 * NG * stage_b > budget) return cudaSuccess;
+  int NS = (int)((budget - fixed) / stage_b);
+  static const int ns_cap = env_int("MDN_U8ROWS_NS", U8_NS_MAX);   // ring-depth A/B knob
+  if (NS > U8_NS_MAX) NS = U8_NS_MAX;
+  if (NS > ns_cap) NS = ns_cap;
+  NS -= NS % NG;                                    // each group owns its ring slots
+  if (NS < NG) NS = NG;                             // (2 NG stages fit: checked above)
+  CUtensorMap tm;
+  if (!make_tmap(&tm, A, N, lda, 32, 16, R, 1)) return cudaSuccess;
+  RParams rp{};
+  SParams& p = rp.p;
+  p.N = N;
+  p.n_tiles = (N + R - 1) / R;
+  p.ldo = ldo;
+  p.pitch_e = 32;
+  p.stage_b = stage_b;
+  p.NS = NS;
+  if (!enc) {
+    p.M = l->M;
+    p.alpha_eff = l->alpha_eff;
+    p.beta32 = l->beta32;
+    p.lut16 = l->words16;
+  }
+  p.out = out;
+  p.codes = codes;
+  for (int c = 0; c < 8; ++c) host_byte_tree(t, c, &rp.cb[c]);
+  const size_t smem = fixed + (size_t)NS * stage_b;
+  *done = true;
+  if (enc) return launch_u8_rows<1, 0, 0, true>(tm, rp, smem, st);
+  const uintptr_t oa = reinterpret_cast<uintptr_t>(out);
+  const bool vec = l->M == 2 * W2 &&
+                   (W2 % 2 == 0 ? (ldo % 4 == 0 && (oa & 15u) == 0) : (ldo % 2 == 0 && (oa & 7u) == 0));
+  if (W2 == 1)
+    return avg ? (vec ? launch_u8_rows<1, 8, 1, false>(tm, rp, smem, st) : launch_u8_rows<1, 8, 0, false>(tm, rp, smem, st))
+               : (vec ? launch_u8_rows<1, 0, 1, false>(tm, rp, smem, st) : launch_u8_rows<1, 0, 0, false>(tm, rp, smem, st));
+  return avg ? (vec ? launch_u8_rows<2, 8, 1, false>(tm, rp, smem, st) : launch_u8_rows<2, 8, 0, false>(tm, rp, smem, st))
+             : (vec ? launch_u8_rows<2, 0, 1, false>(tm, rp, smem, st) : launch_u8_rows<2, 0, 0, false>(tm, rp, smem, st));
+}
+
 template <class TIn, int C, int W2, int U, int VEC, bool BQ>
 cudaError_t launch(const CUtensorMap& tm, const SParams& p, size_t smem, cudaStream_t st) {
   auto k = k_amm_rt<TIn, 32, C, W2, U, VEC, BQ>;
@@ -617,6 +932,12 @@ static cudaError_t amm_rt(const TreesDev& t, const LutsDev& l, const TIn* A, int
   constexpr int es = sizeof(TIn);
   *done = false;
   if (N > (int64_t)0x7FFFFF00 || !rt_ok(t, l, A, lda, es)) return cudaSuccess;
+  if constexpr (es == 1) {
+    if (knob_bq()) {
+      cudaError_t e = u8_rows(t, &l, A, N, lda, out, ldo, nullptr, st, done);
+      if (*done || e != cudaSuccess) return e;
+    }
+  }
   const int pitch_e = es == 1 ? t.D : t.D + 16 / es;     // must match the kernel's PITCH
   const int stage_b = ((R * pitch_e * es) + 127) & ~127;
   const int W2 = (l.M + 1) / 2;
@@ -676,6 +997,12 @@ static cudaError_t encode_rt(const TreesDev& t, const TIn* A, int64_t N, int64_t
   if ((reinterpret_cast<uintptr_t>(A) & 15u) || (lda * es) % 16) return cudaSuccess;
   if (es == 1 && t.subf_u8 != 1) return cudaSuccess;
   if (reinterpret_cast<uintptr_t>(codes) & (uintptr_t)(t.C / 2 - 1)) return cudaSuccess;
+  if constexpr (es == 1) {
+    if (knob_bq()) {
+      cudaError_t e = u8_rows(t, nullptr, A, N, lda, nullptr, 0, codes, st, done);
+      if (*done || e != cudaSuccess) return e;
+    }
+  }
   const int pitch_e = es == 1 ? t.D : t.D + 16 / es;
   const int stage_b = ((R * pitch_e * es) + 127) & ~127;
   const size_t fixed = 256;                          // barriers only (kernel's OFF_STAGE)
