@@ -584,17 +584,22 @@ __global__ void __launch_bounds__(THREADS, sizeof(TIn) == 1 ? MDN_RT_CTAS_U8 : 1
 #define MDN_U8ROWS_NS_MAX 16
 #endif
 constexpr int U8_NS_MAX = MDN_U8ROWS_NS_MAX;
+#ifndef MDN_U8ROWS_NWK
+#define MDN_U8ROWS_NWK 16      // worker warps of k_u8_rows
+#endif
+constexpr int U8_NWK = MDN_U8ROWS_NWK;
+constexpr int U8_THREADS = 32 * (1 + U8_NWK);
 struct RParams {
   SParams p;
   ByteTree cb[8];   // per codebook; ByteTree::base unused (lane-independent)
 };
 
 template <int C, int W2, int U, int VEC, bool ENC, int DP, int SUBS>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(U8_THREADS, 1)
     k_u8_rows(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ RParams rp) {
   static_assert(C == 8, "codebooks are the 4-byte words of a 32-byte row");
   constexpr int D = 32;
-  constexpr int CPS = R / (32 * SUBS), NG = NWK / CPS;
+  constexpr int CPS = R / (32 * SUBS), NG = U8_NWK / CPS;
   constexpr int LROW = 128;                        // bytes per (c, k, w) table row: 32 lanes
   constexpr int OFF_LUT = 16 * U8_NS_MAX;          // full / empty barriers below
   constexpr int OFF_STAGE = (OFF_LUT + (ENC ? 0 : C * 16 * W2 * LROW) + 127) & ~127;
@@ -792,7 +797,7 @@ template <bool ENC, int U>
 struct U8Cfg {
   static constexpr int SUBS = ENC ? MDN_U8ROWS_SUBS_ENC : (U ? MDN_U8ROWS_SUBS_AVG : MDN_U8ROWS_SUBS);
   static constexpr int DP = ENC ? MDN_U8ROWS_DP_ENC : (U ? MDN_U8ROWS_DP_AVG : MDN_U8ROWS_DP);
-  static constexpr int NG = NWK / (R / (32 * SUBS));   // worker groups rotating over stages
+  static constexpr int NG = U8_NWK / (R / (32 * SUBS));   // worker groups rotating over stages
 };
 
 // Is k_u8_rows applicable? 8-bit rows of 32 bytes, 8 codebooks on the row's
@@ -812,7 +817,7 @@ static cudaError_t launch_u8_rows(const CUtensorMap& tm, const RParams& rp, size
   if (e != cudaSuccess) return e;
   const int64_t cap = (int64_t)dev_info().sms;
   const int64_t grid = rp.p.n_tiles < cap ? rp.p.n_tiles : cap;
-  k<<<(unsigned)grid, THREADS, smem, st>>>(tm, rp);
+  k<<<(unsigned)grid, U8_THREADS, smem, st>>>(tm, rp);
   return cudaGetLastError();
 }
 
