@@ -537,8 +537,11 @@ template <int C, int W, int U, bool VEC, int MIX>
 __global__ void __launch_bounds__(256) k_scan_fast(MDN_SCAN_ARGS) {
   scan_fast_body<C, W, U, VEC, MIX>(lut_g, codes, N, M, sums, out, ldo, a, b, scale, pair, vec_codes);
 }
+#ifndef MDN_SCAN_LB1_TPB
+#define MDN_SCAN_LB1_TPB 256   // threads per block of the wide-table scan (one block per SM)
+#endif
 template <int C, int W, int U, bool VEC, int MIX>
-__global__ void __launch_bounds__(256, 1) k_scan_fast_lb1(MDN_SCAN_ARGS) {
+__global__ void __launch_bounds__(MDN_SCAN_LB1_TPB, 1) k_scan_fast_lb1(MDN_SCAN_ARGS) {
   scan_fast_body<C, W, U, VEC, MIX>(lut_g, codes, N, M, sums, out, ldo, a, b, scale, pair, vec_codes);
 }
 #undef MDN_SCAN_ARGS
@@ -794,18 +797,19 @@ cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int
   // One wave of resident blocks (grid-stride): a grid above the occupancy
   // limit leaves a tail wave running at a fraction of the SM (cls100: 80
   // registers -> 3 blocks/SM, so the old 4/SM grid ran its last quarter alone).
+  const int tpb = scan_lb1<C, W>() ? MDN_SCAN_LB1_TPB : 256;
   int per_sm = 0;
-  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+  cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, tpb, smem);
   if (oe != cudaSuccess) return oe;
   static const int bps = env_int("MDN_SCAN_BPS", 0);   // tuning knob: cap blocks/SM
   if (bps > 0 && per_sm > bps) per_sm = bps;
   if (per_sm < 1) per_sm = 1;
-  int64_t blocks = (N + 255) / 256;
+  int64_t blocks = (N + tpb - 1) / tpb;
   const int64_t cap = (int64_t)dev_info().sms * per_sm;
   if (blocks > cap) blocks = cap;
   const bool pair = l.M % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 7u) == 0;
   const bool vec_codes = (reinterpret_cast<uintptr_t>(codes) & (C == 32 ? 15u : 7u)) == 0;
-  k<<<(unsigned)blocks, 256, smem, s>>>(l.words, codes, N, l.M, sums, out, ldo, l.alpha_eff,
+  k<<<(unsigned)blocks, tpb, smem, s>>>(l.words, codes, N, l.M, sums, out, ldo, l.alpha_eff,
                                         l.beta32, l.U == 0 ? 1 : l.U, pair, vec_codes);
   return cudaGetLastError();
 }

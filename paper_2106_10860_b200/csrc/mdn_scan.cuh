@@ -44,8 +44,20 @@ __device__ __forceinline__ uint32_t mad_add(uint32_t acc, uint32_t x, uint32_t o
   return r;
 }
 
+// Raw-word exact sums (MDN_SCAN_RAW, default). A table word holds 4 columns
+// w = x0 + 2^8 x1 + 2^16 x2 + 2^24 x3; the odd bytes need their own 16-bit
+// lanes, o = prmt(w, 0x4341) = x1 + 2^16 x3, but the even ones need not be
+// split out at all: accumulating the RAW words, sum w = E + 2^8 O (mod 2^32)
+// with E = E0 + 2^16 E2 and O = O1 + 2^16 O3 the even / odd lane sums, so
+// E = sum w - 2^8 O (mod 2^32) is exact once per row and word (every lane
+// sum <= 255 C < 2^16 for C <= 256, so E < 2^32). Per word one PRMT and two
+// accumulations instead of a LOP3 mask, a PRMT and two accumulations.
+#ifndef MDN_SCAN_RAW
+#define MDN_SCAN_RAW 1
+#endif
+
 // MIX (exact mode): 0 = ALU only; k > 0 = every k-th word on the ALU, the rest
-// IMAD adds.
+// IMAD adds (raw form: the odd-lane sums of those words as IMAD adds).
 template <int C, int W, int U, bool UNROLL_G = false, int MIX = 0, class Words>
 __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Words words,
                                           uint32_t (&ae)[W], uint32_t (&ao)[W]) {
@@ -66,7 +78,13 @@ __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Word
 #pragma unroll
         for (int w = 0; w < W; ++w) {
           const uint32_t a = p0[w * 16], b = p1[w * 16];
-          if (MIX == 0 || w % (MIX > 0 ? MIX : 1) == 0) {
+          if constexpr (MDN_SCAN_RAW != 0) {
+            ae[w] += a + b;                            // raw words (ae = sum w until the fix-up)
+            if (MIX == 0 || w % (MIX > 0 ? MIX : 1) == 0)
+              ao[w] += __byte_perm(a, 0u, 0x4341) + __byte_perm(b, 0u, 0x4341);
+            else
+              ao[w] = mad_add(mad_add(ao[w], __byte_perm(a, 0u, 0x4341), one), __byte_perm(b, 0u, 0x4341), one);
+          } else if (MIX == 0 || w % (MIX > 0 ? MIX : 1) == 0) {
             ae[w] += (a & 0x00FF00FFu) + (b & 0x00FF00FFu);
             ao[w] += __byte_perm(a, 0u, 0x4341) + __byte_perm(b, 0u, 0x4341);
           } else {
@@ -75,6 +93,10 @@ __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Word
           }
         }
       }
+    }
+    if constexpr (MDN_SCAN_RAW != 0) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) ae[w] -= ao[w] << 8;   // E = sum w - 2^8 O (mod 2^32)
     }
   } else {
     static_assert((U & (U - 1)) == 0 && C % U == 0, "U must be a power of two dividing C");
