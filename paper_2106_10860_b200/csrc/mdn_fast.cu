@@ -511,15 +511,13 @@ __device__ __forceinline__ void scan_fast_body(const uint32_t* __restrict__ lut_
       load_code_words<C>(codes, row, cw, vec_codes);
     }
     uint32_t ae[W], ao[W];
-    scan_core<C, W, U, PF == 2, MIX>(
-        s_lut,
-        [&](int g) {
-          uint32_t r = cw[0];
+    auto words = [&](int g) {
+      uint32_t r = cw[0];
 #pragma unroll
-          for (int k = 1; k < NW; ++k) r = g == k ? cw[k] : r;   // register select, no local memory
-          return r;
-        },
-        ae, ao);
+      for (int k = 1; k < NW; ++k) r = g == k ? cw[k] : r;   // register select, no local memory
+      return r;
+    };
+    scan_core<C, W, U, PF == 2, MIX>(s_lut, words, ae, ao);
     if (sums) store_sums<W>(sums + row * M, M, scale, ae, ao);
     if (out) store_row<W, VEC>(out + row * ldo, M, ae, ao, a, b, pair);
     if constexpr (PF != 0) {
@@ -538,7 +536,7 @@ __global__ void __launch_bounds__(256) k_scan_fast(MDN_SCAN_ARGS) {
   scan_fast_body<C, W, U, VEC, MIX>(lut_g, codes, N, M, sums, out, ldo, a, b, scale, pair, vec_codes);
 }
 #ifndef MDN_SCAN_LB1_TPB
-#define MDN_SCAN_LB1_TPB 256   // threads per block of the wide-table scan (one block per SM)
+#define MDN_SCAN_LB1_TPB 512   // threads per block of the wide-table scan (one block per SM)
 #endif
 template <int C, int W, int U, bool VEC, int MIX>
 __global__ void __launch_bounds__(MDN_SCAN_LB1_TPB, 1) k_scan_fast_lb1(MDN_SCAN_ARGS) {
@@ -767,13 +765,18 @@ cudaError_t launch_ws_t(const CUtensorMap& tm, const Params& p, int subf, size_t
   return launch_ws_sf<TIn, C, W, U, VEC, ENC, 0>(tm, p, smem, s);
 }
 
-// Exact-mode pipe mix of the standalone scan (mdn_scan.cuh). Measured (same
-// box, rows/s, mix vs ALU-only): cls100 +7%, scale +8%, cls10_c64 +8%,
-// cls10_c16 -6%, C <= 8 unchanged; so the default (-1) mixes for C >= 32.
-// MDN_SCAN_MIX=0 forces ALU-only, 3 forces the mix.
+// Exact-mode pipe mix of the standalone scan (mdn_scan.cuh). With the mask
+// form the mix paid (cls100 +7%, scale +8%, cls10_c64 +8%); with the raw-word
+// form (one PRMT per word) ALU-only is as fast or faster (same box, rows/s,
+// ALU-only vs mix: cls100 5.96 vs 5.91e9, scale 3.89 vs 3.89e10, cls10_c64
+// 2.61 vs 2.43e10, cls10_c16 6.02 vs 5.96e10), so the default is ALU-only.
+// MDN_SCAN_MIX=3 forces the mix (every MDN_SCAN_MIXK-th word on the ALU).
+#ifndef MDN_SCAN_MIXK
+#define MDN_SCAN_MIXK 3   // the mixed form: every MIXK-th word's adds on the ALU pipe
+#endif
 static int scan_mix(int C) {
   static const int v = env_int("MDN_SCAN_MIX", -1);
-  return v < 0 ? (C >= 32 ? 3 : 0) : v;
+  return v < 0 ? 0 : v;
 }
 
 template <int C, int W, int U, bool VEC>
@@ -785,11 +788,11 @@ cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int
   if constexpr (scan_lb1<C, W>()) {
     k = k_scan_fast_lb1<C, W, U, VEC, 0>;
     if constexpr (U == 0)
-      if (scan_mix(C) == 3) k = k_scan_fast_lb1<C, W, U, VEC, 3>;
+      if (scan_mix(C) == 3) k = k_scan_fast_lb1<C, W, U, VEC, MDN_SCAN_MIXK>;
   } else {
     k = k_scan_fast<C, W, U, VEC, 0>;
     if constexpr (U == 0)
-      if (scan_mix(C) == 3) k = k_scan_fast<C, W, U, VEC, 3>;
+      if (scan_mix(C) == 3) k = k_scan_fast<C, W, U, VEC, MDN_SCAN_MIXK>;
   }
   size_t smem = (size_t)C * W * 16 * 4;
   cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
