@@ -485,6 +485,10 @@ def run(args):
     op = args.op
     pq = args.encoder == "pq"
     u8 = A.dtype == torch.uint8
+    # 8-bit rows of 32 bytes on 8 four-byte codebooks run k_u8_rows (mdn_small.cu)
+    # unless MDN_U8_ROWS=0; mdn_amm_variant names the fp32 dispatch only
+    u8_kernel = ("k_u8_rows" if spec.C == 8 and spec.D == 32 and os.environ.get("MDN_U8_ROWS", "1") != "0"
+                 else None)
     amm_fn = mdn.mdn_amm_u8 if u8 else mdn.mdn_amm
     enc_fn = mdn.mdn_encode_u8 if u8 else mdn.mdn_encode
     codes = None
@@ -909,7 +913,8 @@ def run(args):
                          "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": n * bytes_per_row,
                          "kernel": (("ws_cm_gather4" if spec.C >= 16 else "k_amm_cm") if col
-                                    else ("pq" if pq else mdn.mdn_amm_variant(model, luts, spec.D)))
+                                    else ("pq" if pq else u8_kernel if u8 and u8_kernel
+                                          else mdn.mdn_amm_variant(model, luts, spec.D)))
                                    if op == "amm" else op,
                          "frac_of_stream_probe": (achieved_gbs / probe["gbs"]) if probe else None},
             "stream_probe": probe,
