@@ -486,6 +486,59 @@ template <int C, int W>
 constexpr bool scan_lb1() {
   return W >= 8 || C >= 64;
 }
+// Wide-table output rows staged through shared memory (MDN_SCAN_STAGE): with
+// lane = row every float4 store of a warp hit 32 different rows (32 partial
+// sectors per instruction), and those stores share the L1 / shared-memory
+// data path with the table lookups -- the scan's own arithmetic alone reaches
+// 0.94 of the 128 B/clk crossbar, with the per-row stores 0.41
+// (scripts/micro/lds_rate.cu). Staged, each half row set (32 rows x <= 52
+// columns) leaves in coalesced runs of whole rows.
+#ifndef MDN_SCAN_STAGE
+#define MDN_SCAN_STAGE 1
+#endif
+template <int W, bool VEC>
+constexpr bool scan_stage() {
+  return MDN_SCAN_STAGE != 0 && VEC && W >= 8;
+}
+// staging float4 per row: ceil(W / 2) (the larger half) rounded up to odd, so
+// the lanes' row pitches land on distinct 4-bank groups per quarter warp
+template <int W>
+constexpr int scan_stage_pitch() {
+  return ((W + 1) / 2) | 1;
+}
+template <int W>
+constexpr int scan_stage_floats() {
+  return 32 * 4 * scan_stage_pitch<W>();
+}
+
+template <int W, int H0, int NH>
+__device__ __forceinline__ void stage_half(float* __restrict__ stg, float* __restrict__ out, int64_t r0,
+                                           int64_t N, int64_t ldo, const uint32_t (&ae)[W],
+                                           const uint32_t (&ao)[W], float a, float b, int lane) {
+  constexpr int P = scan_stage_pitch<W>();   // lane's row -> stg[lane][j], pitch P float4
+#pragma unroll
+  for (int j = 0; j < NH; ++j) {
+    const int w = H0 + j;
+    float4 f;
+    f.x = __fmaf_rn(a, (float)(ae[w] & 0xFFFFu), b);
+    f.y = __fmaf_rn(a, (float)(ao[w] & 0xFFFFu), b);
+    f.z = __fmaf_rn(a, (float)(ae[w] >> 16), b);
+    f.w = __fmaf_rn(a, (float)(ao[w] >> 16), b);
+    reinterpret_cast<float4*>(stg)[lane * P + j] = f;
+  }
+  __syncwarp();
+  // 32 x NH float4: item i = row i / NH, word i % NH; consecutive lanes write
+  // consecutive 16-B pieces of a row
+#pragma unroll
+  for (int it = 0; it < NH; ++it) {
+    const int i = it * 32 + lane;
+    const int r = i / NH, j = i - r * NH;
+    if (r0 + r < N)
+      *reinterpret_cast<float4*>(out + (r0 + r) * ldo + 4 * (H0 + j)) = reinterpret_cast<const float4*>(stg)[r * P + j];
+  }
+  __syncwarp();
+}
+
 template <int C, int W, int U, bool VEC, int MIX>
 __device__ __forceinline__ void scan_fast_body(const uint32_t* __restrict__ lut_g,
                                                const uint8_t* __restrict__ codes, int64_t N, int M,
@@ -499,6 +552,38 @@ __device__ __forceinline__ void scan_fast_body(const uint32_t* __restrict__ lut_
   __syncthreads();
   constexpr int NW = C >= 8 ? C / 8 : 1;
   constexpr int PF = scan_pf_mode<C, W>();
+  if constexpr (scan_stage<W, VEC>()) {
+    if (out) {
+      // warp-uniform row loop: lanes past N scan code 0 and store nothing
+      constexpr int H = (W + 1) / 2;
+      const int lane = threadIdx.x & 31;
+      float* stg = reinterpret_cast<float*>(smem + (size_t)C * W * 16 * 4) +
+                   (size_t)(threadIdx.x >> 5) * scan_stage_floats<W>();
+      const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+      for (int64_t r0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); r0 < N; r0 += stride) {
+        const int64_t row = r0 + lane;
+        uint32_t cw[NW];
+        if (row < N) {
+          load_code_words<C>(codes, row, cw, vec_codes);
+        } else {
+#pragma unroll
+          for (int g = 0; g < NW; ++g) cw[g] = 0u;
+        }
+        uint32_t ae[W], ao[W];
+        auto words = [&](int g) {
+          uint32_t r = cw[0];
+#pragma unroll
+          for (int k = 1; k < NW; ++k) r = g == k ? cw[k] : r;
+          return r;
+        };
+        scan_core<C, W, U, PF == 2, MIX>(s_lut, words, ae, ao);
+        if (sums && row < N) store_sums<W>(sums + row * M, M, scale, ae, ao);
+        stage_half<W, 0, H>(stg, out, r0, N, ldo, ae, ao, a, b, lane);
+        stage_half<W, H, W - H>(stg, out, r0, N, ldo, ae, ao, a, b, lane);
+      }
+      return;
+    }
+  }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t cw[NW];
@@ -794,13 +879,14 @@ cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int
     if constexpr (U == 0)
       if (scan_mix(C) == 3) k = k_scan_fast<C, W, U, VEC, MDN_SCAN_MIXK>;
   }
+  const int tpb = scan_lb1<C, W>() ? MDN_SCAN_LB1_TPB : 256;
   size_t smem = (size_t)C * W * 16 * 4;
+  if constexpr (scan_stage<W, VEC>()) smem += (size_t)(tpb / 32) * scan_stage_floats<W>() * 4;
   cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (attr_err != cudaSuccess) return attr_err;
   // One wave of resident blocks (grid-stride): a grid above the occupancy
   // limit leaves a tail wave running at a fraction of the SM (cls100: 80
   // registers -> 3 blocks/SM, so the old 4/SM grid ran its last quarter alone).
-  const int tpb = scan_lb1<C, W>() ? MDN_SCAN_LB1_TPB : 256;
   int per_sm = 0;
   cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, tpb, smem);
   if (oe != cudaSuccess) return oe;
