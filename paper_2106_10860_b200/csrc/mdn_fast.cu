@@ -225,6 +225,75 @@ __device__ __forceinline__ uint32_t encode_group(const TIn* __restrict__ rowp,
 // tiles: scan_core of tile t, then the row's columns [16 t, 16 t + 16). The
 // encoders and the code hand-off are unchanged; warp roles are the wide-table
 // ones (E2:S8 from W = 8), since a row then costs ntile times a W-word scan.
+// Wide-table output rows staged through shared memory (MDN_SCAN_STAGE): with
+// lane = row every float4 store of a warp hit 32 different rows (32 partial
+// sectors per instruction), and those stores share the L1 / shared-memory
+// data path with the table lookups -- the scan's own arithmetic alone reaches
+// 0.94 of the 128 B/clk crossbar, with the per-row stores 0.41
+// (scripts/micro/lds_rate.cu). Staged, each half row set (32 rows x <= 52
+// columns) leaves in coalesced runs of whole rows.
+#ifndef MDN_SCAN_STAGE
+#define MDN_SCAN_STAGE 1
+#endif
+template <int W, bool VEC>
+constexpr bool scan_stage() {
+  return MDN_SCAN_STAGE != 0 && VEC && W >= 8;
+}
+// staging float4 per row: ceil(W / 2) (the larger half) rounded up to odd, so
+// the lanes' row pitches land on distinct 4-bank groups per quarter warp
+template <int W>
+constexpr int scan_stage_pitch() {
+  return ((W + 1) / 2) | 1;
+}
+template <int W>
+constexpr int scan_stage_floats() {
+  return 32 * 4 * scan_stage_pitch<W>();
+}
+// Column-major fused kernel (k_amm_ws<..., CM>), wide tables: its 8 scanner
+// warps stage their rows in 4 parts of CM_PART words (odd), which keeps two
+// R = 128 gather4 stages in shared memory (MDN_CM_STAGE=0 at build: off).
+#ifndef MDN_CM_STAGE
+#define MDN_CM_STAGE 1
+#endif
+template <int W>
+constexpr int CM_PART() {
+  return ((W + 3) / 4) | 1;
+}
+template <int W, bool ENC_ONLY, bool CMV>
+constexpr int cm_ostg_bytes() {
+  return MDN_CM_STAGE != 0 && CMV && !ENC_ONLY && W >= 8 && W - 3 * CM_PART<W>() > 0 ? 8 * 32 * 16 * CM_PART<W>() : 0;
+}
+
+// One part of a warp's 32 output rows (words [H0, H0 + NH)) through the
+// warp's staging buffer (pitch P float4 per row, P odd).
+template <int W, int H0, int NH, int P>
+__device__ __forceinline__ void stage_part(float* __restrict__ stg, float* __restrict__ out, int64_t r0,
+                                           int64_t N, int64_t ldo, const uint32_t (&ae)[W],
+                                           const uint32_t (&ao)[W], float a, float b, int lane) {
+  static_assert(NH <= P && (P & 1), "part must fit the odd row pitch");
+#pragma unroll
+  for (int j = 0; j < NH; ++j) {
+    const int w = H0 + j;
+    float4 f;
+    f.x = __fmaf_rn(a, (float)(ae[w] & 0xFFFFu), b);
+    f.y = __fmaf_rn(a, (float)(ao[w] & 0xFFFFu), b);
+    f.z = __fmaf_rn(a, (float)(ae[w] >> 16), b);
+    f.w = __fmaf_rn(a, (float)(ao[w] >> 16), b);
+    reinterpret_cast<float4*>(stg)[lane * P + j] = f;
+  }
+  __syncwarp();
+  // 32 x NH float4: item i = row i / NH, word i % NH; consecutive lanes write
+  // consecutive 16-B pieces of a row
+#pragma unroll
+  for (int it = 0; it < NH; ++it) {
+    const int i = it * 32 + lane;
+    const int r = i / NH, j = i - r * NH;
+    if (r0 + r < N)
+      *reinterpret_cast<float4*>(out + (r0 + r) * ldo + 4 * (H0 + j)) = reinterpret_cast<const float4*>(stg)[r * P + j];
+  }
+  __syncwarp();
+}
+
 template <class TIn, int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF, bool PROBE = false,
           bool TILED = false>
 __global__ void __launch_bounds__(Roles<(TILED ? 8 : W), ENC_ONLY, SUBF == CM>::THREADS, 1)
@@ -249,7 +318,9 @@ __global__ void __launch_bounds__(Roles<(TILED ? 8 : W), ENC_ONLY, SUBF == CM>::
   constexpr int OFF_COLS = OFF_BASE + C * 4;
   constexpr int OFF_LUT = (OFF_COLS + (SUBF == CM ? 4 * C * 4 : 0) + 15) & ~15;
   constexpr int OFF_CODES = OFF_LUT + (ENC_ONLY || TILED ? 0 : C * W * 16 * 4);
-  constexpr int OFF_STAGE = (OFF_CODES + (ENC_ONLY ? 0 : NB * BR * CBW * 4) + 127) & ~127;
+  // column-major wide tables: the scanner warps' output staging (cm_ostg_bytes)
+  constexpr int OFF_OSTG = (OFF_CODES + (ENC_ONLY ? 0 : NB * BR * CBW * 4) + 15) & ~15;
+  constexpr int OFF_STAGE = (OFF_OSTG + cm_ostg_bytes<W, ENC_ONLY, SUBF == CM>() + 127) & ~127;
   float* s_thr = reinterpret_cast<float*>(smem + OFF_THR);
   int* s_off = reinterpret_cast<int*>(smem + OFF_OFF);
   int* s_base = reinterpret_cast<int*>(smem + OFF_BASE);
@@ -422,8 +493,19 @@ __global__ void __launch_bounds__(Roles<(TILED ? 8 : W), ENC_ONLY, SUBF == CM>::
           scan_core<C, W, U, false, (SUBF == CM && W >= 8) ? MDN_CM_MIX : 0>(s_lut, [&](int g) { return myc[g]; }, ae, ao);
         }
         if (k == KR - 1) mbar_arrive(&cempty[b]);
-        if (row < p.N)
+        if constexpr (VEC && cm_ostg_bytes<W, ENC_ONLY, SUBF == CM>() > 0) {
+          // coalesced row stores in 4 parts of <= CM_PART words (see scan_stage)
+          constexpr int Q = CM_PART<W>();
+          float* stg = reinterpret_cast<float*>(smem + OFF_OSTG) + (size_t)(stid >> 5) * 32 * 4 * Q;
+          const int64_t r0 = row - (stid & 31);
+          const int lane = stid & 31;
+          stage_part<W, 0, Q, Q>(stg, p.out, r0, p.N, p.ldo, ae, ao, p.alpha_eff, p.beta32, lane);
+          stage_part<W, Q, Q, Q>(stg, p.out, r0, p.N, p.ldo, ae, ao, p.alpha_eff, p.beta32, lane);
+          stage_part<W, 2 * Q, Q, Q>(stg, p.out, r0, p.N, p.ldo, ae, ao, p.alpha_eff, p.beta32, lane);
+          stage_part<W, 3 * Q, W - 3 * Q, Q>(stg, p.out, r0, p.N, p.ldo, ae, ao, p.alpha_eff, p.beta32, lane);
+        } else if (row < p.N) {
           store_row<W, VEC>(p.out + row * p.ldo, p.M, ae, ao, p.alpha_eff, p.beta32, p.pair);
+        }
       }
     }
   }
@@ -486,59 +568,6 @@ template <int C, int W>
 constexpr bool scan_lb1() {
   return W >= 8 || C >= 64;
 }
-// Wide-table output rows staged through shared memory (MDN_SCAN_STAGE): with
-// lane = row every float4 store of a warp hit 32 different rows (32 partial
-// sectors per instruction), and those stores share the L1 / shared-memory
-// data path with the table lookups -- the scan's own arithmetic alone reaches
-// 0.94 of the 128 B/clk crossbar, with the per-row stores 0.41
-// (scripts/micro/lds_rate.cu). Staged, each half row set (32 rows x <= 52
-// columns) leaves in coalesced runs of whole rows.
-#ifndef MDN_SCAN_STAGE
-#define MDN_SCAN_STAGE 1
-#endif
-template <int W, bool VEC>
-constexpr bool scan_stage() {
-  return MDN_SCAN_STAGE != 0 && VEC && W >= 8;
-}
-// staging float4 per row: ceil(W / 2) (the larger half) rounded up to odd, so
-// the lanes' row pitches land on distinct 4-bank groups per quarter warp
-template <int W>
-constexpr int scan_stage_pitch() {
-  return ((W + 1) / 2) | 1;
-}
-template <int W>
-constexpr int scan_stage_floats() {
-  return 32 * 4 * scan_stage_pitch<W>();
-}
-
-template <int W, int H0, int NH>
-__device__ __forceinline__ void stage_half(float* __restrict__ stg, float* __restrict__ out, int64_t r0,
-                                           int64_t N, int64_t ldo, const uint32_t (&ae)[W],
-                                           const uint32_t (&ao)[W], float a, float b, int lane) {
-  constexpr int P = scan_stage_pitch<W>();   // lane's row -> stg[lane][j], pitch P float4
-#pragma unroll
-  for (int j = 0; j < NH; ++j) {
-    const int w = H0 + j;
-    float4 f;
-    f.x = __fmaf_rn(a, (float)(ae[w] & 0xFFFFu), b);
-    f.y = __fmaf_rn(a, (float)(ao[w] & 0xFFFFu), b);
-    f.z = __fmaf_rn(a, (float)(ae[w] >> 16), b);
-    f.w = __fmaf_rn(a, (float)(ao[w] >> 16), b);
-    reinterpret_cast<float4*>(stg)[lane * P + j] = f;
-  }
-  __syncwarp();
-  // 32 x NH float4: item i = row i / NH, word i % NH; consecutive lanes write
-  // consecutive 16-B pieces of a row
-#pragma unroll
-  for (int it = 0; it < NH; ++it) {
-    const int i = it * 32 + lane;
-    const int r = i / NH, j = i - r * NH;
-    if (r0 + r < N)
-      *reinterpret_cast<float4*>(out + (r0 + r) * ldo + 4 * (H0 + j)) = reinterpret_cast<const float4*>(stg)[r * P + j];
-  }
-  __syncwarp();
-}
-
 template <int C, int W, int U, bool VEC, int MIX>
 __device__ __forceinline__ void scan_fast_body(const uint32_t* __restrict__ lut_g,
                                                const uint8_t* __restrict__ codes, int64_t N, int M,
@@ -578,8 +607,8 @@ __device__ __forceinline__ void scan_fast_body(const uint32_t* __restrict__ lut_
         };
         scan_core<C, W, U, PF == 2, MIX>(s_lut, words, ae, ao);
         if (sums && row < N) store_sums<W>(sums + row * M, M, scale, ae, ao);
-        stage_half<W, 0, H>(stg, out, r0, N, ldo, ae, ao, a, b, lane);
-        stage_half<W, H, W - H>(stg, out, r0, N, ldo, ae, ao, a, b, lane);
+        stage_part<W, 0, H, scan_stage_pitch<W>()>(stg, out, r0, N, ldo, ae, ao, a, b, lane);
+        stage_part<W, H, W - H, scan_stage_pitch<W>()>(stg, out, r0, N, ldo, ae, ao, a, b, lane);
       }
       return;
     }
@@ -1149,7 +1178,9 @@ static Geometry plan_cm(int C, int W, int n_cols, bool enc_only) {
   g.pad_e = 0;
   const int CBW = C >= 8 ? C / 8 : 1;
   size_t fixed = BAR_BYTES + thr_base(C) * 4 + off_base(C) * 4 + C * 4 + 4 * C * 4 + 16;
-  if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4;
+  if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4 + 16;
+  if (!enc_only && MDN_CM_STAGE != 0 && W >= 8 && W - 3 * (((W + 3) / 4) | 1) > 0)
+    fixed += (size_t)8 * 32 * 16 * (((W + 3) / 4) | 1);   // cm_ostg_bytes (scanner output staging)
   fixed = (fixed + 127) & ~size_t(127);
   const size_t budget = (size_t)dev_info().smem_optin;
   // Largest R with >= 2 stages: the column boxes are R * 4 bytes and the TMA
