@@ -658,6 +658,103 @@ __global__ void __launch_bounds__(MDN_SCAN_LB1_TPB, 1) k_scan_fast_lb1(MDN_SCAN_
 }
 #undef MDN_SCAN_ARGS
 
+// Wide-table mdn_scan with TMA tensor stores of the staged rows
+// (MDN_SCAN_TSTORE). The staging buffer of a warp is already a dense box
+// (32 rows x P float4, P odd), so instead of reading it back (LDS) and
+// storing it from the registers (STG through the L1 path the lookups use),
+// one lane hands the box to the TMA unit: per 32 rows and part, one
+// instruction instead of P LDS.128 + P STG.128 per lane, and the rows past N
+// are clipped by the tensor map. Part 1 starts at word W - P (it overlaps
+// part 0 by 2P - W words, written twice with the same values). NBUF buffers
+// per warp: with 2 the second part never waits for the first part's read.
+// Same box, cls100 rows/s (exact / avg): LDS + STG readback 6.89 / 4.87e9,
+// TMA stores with 1 buffer (512 threads) 8.10 / 5.66e9, with 2 buffers (384
+// threads) 8.09 / 5.63e9; kept: 1 buffer. MDN_SCAN_TSTORE=0 (build flag)
+// restores the readback.
+#ifndef MDN_SCAN_TSTORE
+#define MDN_SCAN_TSTORE 1
+#endif
+#ifndef MDN_SCAN_TS_NBUF
+#define MDN_SCAN_TS_NBUF 1
+#endif
+#ifndef MDN_SCAN_TS_TPB
+#define MDN_SCAN_TS_TPB (MDN_SCAN_TS_NBUF == 1 ? 512 : 384)
+#endif
+template <int C, int W, int U, int MIX>
+__global__ void __launch_bounds__(MDN_SCAN_TS_TPB, 1)
+    k_scan_ts(const __grid_constant__ CUtensorMap om, const uint32_t* __restrict__ lut_g,
+              const uint8_t* __restrict__ codes, int64_t N, int M, int32_t* __restrict__ sums,
+              float a, float b, int scale, bool vec_codes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem);
+  for (int i = threadIdx.x; i < C * W * 4; i += blockDim.x)
+    reinterpret_cast<uint4*>(s_lut)[i] = reinterpret_cast<const uint4*>(lut_g)[i];
+  __syncthreads();
+  constexpr int NW = C >= 8 ? C / 8 : 1;
+  constexpr int PF = scan_pf_mode<C, W>();
+  constexpr int P = scan_stage_pitch<W>();
+  constexpr int H1 = W - P;
+  static_assert(H1 > 0 && H1 <= P, "two parts of P words cover the row");
+  constexpr int NBUF = MDN_SCAN_TS_NBUF;
+  const int lane = threadIdx.x & 31;
+  float* stg0 = reinterpret_cast<float*>(smem + (size_t)C * W * 16 * 4) +
+                (size_t)(threadIdx.x >> 5) * NBUF * scan_stage_floats<W>();
+  float* stg1 = stg0 + (NBUF - 1) * scan_stage_floats<W>();
+  auto part = [&](float* stg, int h0, const uint32_t(&ae)[W], const uint32_t(&ao)[W]) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int w = h0 + j;
+      float4 f;
+      f.x = __fmaf_rn(a, (float)(ae[w] & 0xFFFFu), b);
+      f.y = __fmaf_rn(a, (float)(ao[w] & 0xFFFFu), b);
+      f.z = __fmaf_rn(a, (float)(ae[w] >> 16), b);
+      f.w = __fmaf_rn(a, (float)(ao[w] >> 16), b);
+      reinterpret_cast<float4*>(stg)[lane * P + j] = f;
+    }
+  };
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); r0 < N; r0 += stride) {
+    const int64_t row = r0 + lane;
+    uint32_t cw[NW];
+    if (row < N) {
+      load_code_words<C>(codes, row, cw, vec_codes);
+    } else {
+#pragma unroll
+      for (int g = 0; g < NW; ++g) cw[g] = 0u;
+    }
+    uint32_t ae[W], ao[W];
+    auto words = [&](int g) {
+      uint32_t r = cw[0];
+#pragma unroll
+      for (int k = 1; k < NW; ++k) r = g == k ? cw[k] : r;
+      return r;
+    };
+    scan_core<C, W, U, PF == 2, MIX>(s_lut, words, ae, ao);
+    if (sums && row < N) store_sums<W>(sums + row * M, M, scale, ae, ao);
+    // part 0: its buffer's previous store must have been read (NBUF = 2: the
+    // one group allowed to be pending is the other buffer's)
+    if (lane == 0) bulk_wait_read<NBUF - 1>();
+    __syncwarp();
+    part(stg0, 0, ae, ao);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(&om, stg0, 0, (int)r0);
+      bulk_commit();
+      bulk_wait_read<NBUF - 1>();
+    }
+    __syncwarp();
+    part(stg1, H1, ae, ao);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(&om, stg1, 4 * H1, (int)r0);
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
 // mdn_scan for table widths without a compiled kernel: the tables cut into
 // ntile column tiles of WT words ([tile][c][WT][16] in shared memory, words
 // past the width zero); a thread's row walks the tiles with its code words
@@ -857,6 +954,18 @@ bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_tmap_out(CUtensorMap* m, float* out, int64_t N, int M, int64_t ldo, int bw, int bh) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
+  cuuint64_t strides[1] = {(cuuint64_t)ldo * 4};
+  cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <class TIn, int C, int W, int U, bool VEC, bool ENC, int SUBF, bool PROBE = false,
           bool TILED = false>
 cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
@@ -898,6 +1007,29 @@ cudaError_t launch_scan_t(const LutsDev& l, const uint8_t* codes, int64_t N, int
                           float* out, int64_t ldo, cudaStream_t s) {
   using KFn = void (*)(const uint32_t*, const uint8_t*, int64_t, int, int32_t*, float*, int64_t, float,
                       float, int, bool, bool);
+  if constexpr (MDN_SCAN_TSTORE != 0 && scan_stage<W, VEC>()) {
+    constexpr int P = scan_stage_pitch<W>();
+    CUtensorMap om;
+    if (out && N > 0 && scan_mix(C) == 0 && make_tmap_out(&om, out, N, l.M, ldo, 4 * P, 32)) {
+      auto kt = k_scan_ts<C, W, U, 0>;
+      constexpr int tpb = MDN_SCAN_TS_TPB;
+      const size_t smem =
+          (size_t)C * W * 16 * 4 + (size_t)(tpb / 32) * MDN_SCAN_TS_NBUF * scan_stage_floats<W>() * 4;
+      cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kt), smem);
+      if (e != cudaSuccess) return e;
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kt, tpb, smem);
+      if (e != cudaSuccess) return e;
+      if (per_sm < 1) per_sm = 1;
+      int64_t blocks = (N + tpb - 1) / tpb;
+      const int64_t cap = (int64_t)dev_info().sms * per_sm;
+      if (blocks > cap) blocks = cap;
+      const bool vec_codes = (reinterpret_cast<uintptr_t>(codes) & (C == 32 ? 15u : 7u)) == 0;
+      kt<<<(unsigned)blocks, tpb, smem, s>>>(om, l.words, codes, N, l.M, sums, l.alpha_eff, l.beta32,
+                                             l.U == 0 ? 1 : l.U, vec_codes);
+      return cudaGetLastError();
+    }
+  }
   KFn k;
   if constexpr (scan_lb1<C, W>()) {
     k = k_scan_fast_lb1<C, W, U, VEC, 0>;

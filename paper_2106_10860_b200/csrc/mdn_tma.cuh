@@ -84,6 +84,28 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// 2-D TMA tensor store (shared -> global, bulk-group completion): the box at
+// (x, y) of the map's tensor is written from dense shared memory at src;
+// elements outside the tensor (rows >= N, columns >= M) are not written.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(su32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N of this thread's committed bulk groups still READING shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// all of this thread's bulk groups complete (writes performed)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// this thread's generic-proxy shared-memory writes visible to the async proxy (TMA)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Host helpers (mdn_fast.cu).
 struct DevInfo {
   int sms = 148;
@@ -94,6 +116,8 @@ DevInfo dev_info();
 // size): the attribute costs ~1 us per call, more than a small launch.
 cudaError_t ensure_smem(const void* kernel, size_t smem);
 bool make_tmap(CUtensorMap* m, const void* A, int64_t N, int64_t lda, int D, int SW, int R, int es);
+// fp32 output [N][M] at row pitch ldo (floats), stored in boxes of bw columns x bh rows
+bool make_tmap_out(CUtensorMap* m, float* out, int64_t N, int M, int64_t ldo, int bw, int bh);
 int knob_hint();
 bool knob_bq();
 int env_int(const char* name, int dflt);   // tuning knobs (mdn_fast.cu)

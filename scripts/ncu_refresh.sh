@@ -21,13 +21,13 @@ bash scripts/ncu_capture.sh \
   cls100_encode_exact k_amm_ws --config cls100 --op encode -- \
   image_encode_exact k_amm_rt --config image --op encode -- \
   image_u8_encode_exact k_u8_rows --config image_u8 --op encode -- \
-  cls100_scan_exact k_scan_fast --config cls100 --op scan -- \
+  cls100_scan_exact k_scan_ts --config cls100 --op scan -- \
   image_scan_exact k_scan_fast --config image --op scan -- \
   cls100_encode_pq_exact k_encode_pq --config cls100 --op encode --encoder pq -- \
   scale_encode_pq_exact k_encode_pq --config scale --op encode --encoder pq -- \
   cls10_c16_encode_pq_exact k_encode_pq --config cls10_c16 --op encode --encoder pq -- \
   scale_scan_exact k_scan_fast --config scale --op scan -- \
-  cls100_scan_avg k_scan_fast --config cls100 --op scan --mode avg
+  cls100_scan_avg k_scan_ts --config cls100 --op scan --mode avg
 # the pipeline probe (mdn_amm_probe) of the headline config: same kernel name
 # as the fused kernel, told apart by its template arguments
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
