@@ -259,6 +259,14 @@ template <int W>
 constexpr int CM_PART() {
   return ((W + 3) / 4) | 1;
 }
+// Their parts leave by TMA tensor stores (MDN_CM_TSTORE, as k_scan_ts; one
+// buffer per warp, each part waits for the previous part's read). Same box,
+// cls100 column-major rows/s (exact / avg): LDS + STG readback 5.01 / 3.88e9
+// (0.698 of HBM), TMA stores 5.60 / 4.22e9 (0.779); MDN_CM_TSTORE=0 restores
+// the readback.
+#ifndef MDN_CM_TSTORE
+#define MDN_CM_TSTORE 1
+#endif
 template <int W, bool ENC_ONLY, bool CMV>
 constexpr int cm_ostg_bytes() {
   return MDN_CM_STAGE != 0 && CMV && !ENC_ONLY && W >= 8 && W - 3 * CM_PART<W>() > 0 ? 8 * 32 * 16 * CM_PART<W>() : 0;
@@ -297,7 +305,8 @@ __device__ __forceinline__ void stage_part(float* __restrict__ stg, float* __res
 template <class TIn, int C, int W, int U, bool VEC, bool ENC_ONLY, int SUBF, bool PROBE = false,
           bool TILED = false>
 __global__ void __launch_bounds__(Roles<(TILED ? 8 : W), ENC_ONLY, SUBF == CM>::THREADS, 1)
-    k_amm_ws(const __grid_constant__ CUtensorMap tmap, const Params p) {
+    k_amm_ws(const __grid_constant__ CUtensorMap tmap, const Params p,
+             const __grid_constant__ CUtensorMap omap) {
   constexpr int G = C >= 8 ? 8 : C;      // codebooks per encoder unit (one code word)
   constexpr int NG = C / G;
   constexpr int CBW = NG;                // code words per row
@@ -319,7 +328,8 @@ __global__ void __launch_bounds__(Roles<(TILED ? 8 : W), ENC_ONLY, SUBF == CM>::
   constexpr int OFF_LUT = (OFF_COLS + (SUBF == CM ? 4 * C * 4 : 0) + 15) & ~15;
   constexpr int OFF_CODES = OFF_LUT + (ENC_ONLY || TILED ? 0 : C * W * 16 * 4);
   // column-major wide tables: the scanner warps' output staging (cm_ostg_bytes)
-  constexpr int OFF_OSTG = (OFF_CODES + (ENC_ONLY ? 0 : NB * BR * CBW * 4) + 15) & ~15;
+  // (128-B aligned for the TMA stores of MDN_CM_TSTORE; plan_cm budgets the slack)
+  constexpr int OFF_OSTG = (OFF_CODES + (ENC_ONLY ? 0 : NB * BR * CBW * 4) + 127) & ~127;
   constexpr int OFF_STAGE = (OFF_OSTG + cm_ostg_bytes<W, ENC_ONLY, SUBF == CM>() + 127) & ~127;
   float* s_thr = reinterpret_cast<float*>(smem + OFF_THR);
   int* s_off = reinterpret_cast<int*>(smem + OFF_OFF);
@@ -499,6 +509,34 @@ __global__ void __launch_bounds__(Roles<(TILED ? 8 : W), ENC_ONLY, SUBF == CM>::
           float* stg = reinterpret_cast<float*>(smem + OFF_OSTG) + (size_t)(stid >> 5) * 32 * 4 * Q;
           const int64_t r0 = row - (stid & 31);
           const int lane = stid & 31;
+          if constexpr (MDN_CM_TSTORE != 0) {
+            // TMA tensor stores of the 4 parts (last part starts at W - Q)
+            auto tpart = [&](int h0) {
+              if (lane == 0) bulk_wait_read<0>();
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < Q; ++j) {
+                const int w = h0 + j;
+                float4 f;
+                f.x = __fmaf_rn(p.alpha_eff, (float)(ae[w] & 0xFFFFu), p.beta32);
+                f.y = __fmaf_rn(p.alpha_eff, (float)(ao[w] & 0xFFFFu), p.beta32);
+                f.z = __fmaf_rn(p.alpha_eff, (float)(ae[w] >> 16), p.beta32);
+                f.w = __fmaf_rn(p.alpha_eff, (float)(ao[w] >> 16), p.beta32);
+                reinterpret_cast<float4*>(stg)[lane * Q + j] = f;
+              }
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&omap, stg, 4 * h0, (int)r0);
+                bulk_commit();
+              }
+            };
+            tpart(0);
+            tpart(Q);
+            tpart(2 * Q);
+            tpart(W - Q);
+            continue;
+          }
           stage_part<W, 0, Q, Q>(stg, p.out, r0, p.N, p.ldo, ae, ao, p.alpha_eff, p.beta32, lane);
           stage_part<W, Q, Q, Q>(stg, p.out, r0, p.N, p.ldo, ae, ao, p.alpha_eff, p.beta32, lane);
           stage_part<W, 2 * Q, Q, Q>(stg, p.out, r0, p.N, p.ldo, ae, ao, p.alpha_eff, p.beta32, lane);
@@ -508,6 +546,8 @@ __global__ void __launch_bounds__(Roles<(TILED ? 8 : W), ENC_ONLY, SUBF == CM>::
         }
       }
     }
+    if constexpr (MDN_CM_TSTORE != 0 && VEC && cm_ostg_bytes<W, ENC_ONLY, SUBF == CM>() > 0)
+      if ((stid & 31) == 0) bulk_wait_all();
   }
 }
 
@@ -968,12 +1008,13 @@ bool make_tmap_out(CUtensorMap* m, float* out, int64_t N, int M, int64_t ldo, in
 
 template <class TIn, int C, int W, int U, bool VEC, bool ENC, int SUBF, bool PROBE = false,
           bool TILED = false>
-cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s) {
+cudaError_t launch_ws_sf(const CUtensorMap& tm, const Params& p, size_t smem, cudaStream_t s,
+                         const CUtensorMap* om = nullptr) {
   auto k = k_amm_ws<TIn, C, W, U, VEC, ENC, SUBF, PROBE, TILED>;
   cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(k), smem);
   if (attr_err != cudaSuccess) return attr_err;
   int64_t grid = p.n_tiles < dev_info().sms ? p.n_tiles : dev_info().sms;
-  k<<<(unsigned)grid, Roles<(TILED ? 8 : W), ENC, SUBF == CM>::THREADS, smem, s>>>(tm, p);
+  k<<<(unsigned)grid, Roles<(TILED ? 8 : W), ENC, SUBF == CM>::THREADS, smem, s>>>(tm, p, om ? *om : tm);
   return cudaGetLastError();
 }
 
@@ -1312,7 +1353,7 @@ static Geometry plan_cm(int C, int W, int n_cols, bool enc_only) {
   size_t fixed = BAR_BYTES + thr_base(C) * 4 + off_base(C) * 4 + C * 4 + 4 * C * 4 + 16;
   if (!enc_only) fixed += (size_t)C * W * 16 * 4 + (size_t)NB * BR * CBW * 4 + 16;
   if (!enc_only && MDN_CM_STAGE != 0 && W >= 8 && W - 3 * (((W + 3) / 4) | 1) > 0)
-    fixed += (size_t)8 * 32 * 16 * (((W + 3) / 4) | 1);   // cm_ostg_bytes (scanner output staging)
+    fixed += (size_t)8 * 32 * 16 * (((W + 3) / 4) | 1) + 128;   // cm_ostg_bytes (scanner output staging) + alignment
   fixed = (fixed + 127) & ~size_t(127);
   const size_t budget = (size_t)dev_info().smem_optin;
   // Largest R with >= 2 stages: the column boxes are R * 4 bytes and the TMA
@@ -1379,11 +1420,16 @@ cudaError_t launch_amm_ws_cm(const TreesDev& t, const LutsDev& l, const float* A
   p.lut = l.words;
   p.out = out;
   const bool vec = l.M % 4 == 0 && ldo % 4 == 0 && aligned16(out);
+  // wide tables, VEC: the scanners' staged parts leave by TMA (MDN_CM_TSTORE)
+  CUtensorMap om;
+  const bool ts = MDN_CM_TSTORE != 0 && vec && MDN_CM_STAGE != 0 && l.W >= 8 &&
+                  l.W - 3 * (((l.W + 3) / 4) | 1) > 0;
+  if (ts && !make_tmap_out(&om, out, N, l.M, ldo, 4 * (((l.W + 3) / 4) | 1), 32)) return cudaSuccess;
   *done = true;
 #define X(c, w, u)                                                                   \
   if constexpr (c >= 16)                                                             \
     if (t.C == c && l.W == w && l.U == u)                                            \
-      return vec ? launch_ws_sf<float, c, w, u, true, false, CM>(tm, p, g.smem, s)   \
+      return vec ? launch_ws_sf<float, c, w, u, true, false, CM>(tm, p, g.smem, s, ts ? &om : nullptr) \
                  : launch_ws_sf<float, c, w, u, false, false, CM>(tm, p, g.smem, s);
   MDN_FAST_COMBOS(X)
 #undef X
