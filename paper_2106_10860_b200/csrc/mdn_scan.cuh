@@ -29,6 +29,30 @@ __device__ __forceinline__ uint32_t avg8(uint32_t a, uint32_t b) {
   return (a | b) - (x >> 1);
 }
 
+// Three-instruction form (MDN_AVG_LEA, default). On complemented bytes the
+// rounded-up average is the rounded-down one: 255 - mu(a, b) = floor(((255 -
+// a) + (255 - b)) / 2) = (a' & b') + (((a' ^ b') & 0xFE..) >> 1), and ptxas
+// fuses the shift and the add into one LEA.HI (the subtraction of avg8 does
+// not fuse): LOP3, LOP3, LEA.HI. avg8_c1 takes raw a, b (a' & b' = ~(a | b),
+// a' ^ b' = a ^ b) and returns the complemented average; avg8_c takes and
+// returns complemented values. The tree's root stays complemented and is
+// SUBTRACTED from lane sums pre-loaded with 255 per block (scan_core), so no
+// instruction is spent on complementing. Bit-identical to avg8 (R16/R17).
+#ifndef MDN_AVG_LEA
+#define MDN_AVG_LEA 1
+#endif
+__device__ __forceinline__ uint32_t avg8_c1(uint32_t a, uint32_t b) {
+  uint32_t x, n;
+  asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(x) : "r"(a), "r"(b), "r"(0xFEFEFEFEu));
+  asm("lop3.b32 %0, %1, %2, %3, 0x03;" : "=r"(n) : "r"(a), "r"(b), "r"(0u));
+  return n + (x >> 1);
+}
+__device__ __forceinline__ uint32_t avg8_c(uint32_t a, uint32_t b) {
+  uint32_t x;
+  asm("lop3.b32 %0, %1, %2, %3, 0x28;" : "=r"(x) : "r"(a), "r"(b), "r"(0xFEFEFEFEu));
+  return (a & b) + (x >> 1);
+}
+
 // Pipe balancing. The exact accumulate is LOP/PRMT (split a word into its
 // even and odd byte lanes) + adds, all on the ALU pipe by default, which then
 // saturates (ncu: ALU 73%, issue 51% on cls100 mdn_scan) while the FMA pipe
@@ -101,6 +125,16 @@ __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Word
   } else {
     static_assert((U & (U - 1)) == 0 && C % U == 0, "U must be a power of two dividing C");
     constexpr int NBU = UNROLL_G ? C / U : 1;
+    constexpr bool CPL = MDN_AVG_LEA != 0 && U >= 2;   // complemented tree roots
+    if constexpr (CPL) {
+      // every 16-bit lane starts 255 per block ahead and loses 255 - mu per
+      // block: it never goes negative, so no lane borrows from its neighbour
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        ae[w] += (uint32_t)(255 * (C / U)) * 0x00010001u;
+        ao[w] += (uint32_t)(255 * (C / U)) * 0x00010001u;
+      }
+    }
 #pragma unroll NBU
     for (int blk = 0; blk < C / U; ++blk) {
       const uint32_t* p[U];
@@ -125,9 +159,17 @@ __device__ __forceinline__ void scan_core(const uint32_t* __restrict__ lut, Word
 #pragma unroll
         for (int s = 1; s < U; s *= 2)
 #pragma unroll
-          for (int i = 0; i < U; i += 2 * s) v[i] = avg8(v[i], v[i + s]);
-        ae[w] += v[0] & 0x00FF00FFu;
-        ao[w] += __byte_perm(v[0], 0u, 0x4341);
+          for (int i = 0; i < U; i += 2 * s) {
+            if constexpr (!CPL) v[i] = avg8(v[i], v[i + s]);
+            else v[i] = s == 1 ? avg8_c1(v[i], v[i + s]) : avg8_c(v[i], v[i + s]);
+          }
+        if constexpr (CPL) {
+          ae[w] -= v[0] & 0x00FF00FFu;
+          ao[w] -= __byte_perm(v[0], 0u, 0x4341);
+        } else {
+          ae[w] += v[0] & 0x00FF00FFu;
+          ao[w] += __byte_perm(v[0], 0u, 0x4341);
+        }
       }
     }
   }
